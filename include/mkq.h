@@ -1,0 +1,214 @@
+/*
+ * mkq.h -- C ABI of the B200-native MKQ-BERT W4A4 inference hot path
+ *          (arXiv 2203.13483, "MKQ-BERT: Quantized BERT with 4-bits Weights
+ *          and Activations").  Library: paper_2203_13483_b200/libmkq.so.
+ *
+ * Citations: "P:n" = line n of the paper text;
+ * "Rn" = a reading of the paper recorded in DESIGN.md §3; "§8a-x" = a row of
+ * the hot-path scope table in SURVEY.md §8(a).
+ *
+ * Conventions shared by every entry point
+ * ----------------------------------------
+ *  - Pointers marked [device] are CUDA device pointers; pointers marked
+ *    [host] are read during the call only.  The caller owns every buffer; the
+ *    library never allocates, frees or synchronizes device memory, except a
+ *    process-wide cache of TMA descriptors keyed by (pointer, shape, stride)
+ *    (descriptors encode no contents, so allocator reuse is safe).
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).  Every call
+ *    only enqueues work on it and returns; the sequence is CUDA-graph
+ *    capturable.  Asynchronous faults surface at the caller's next sync.
+ *  - Matrices are row-major.  "K-major" operands store the reduction index
+ *    contiguously.  int4 codes are packed two per byte: element k of a row is
+ *    in byte k/2, even k in the low nibble, two's complement (layout D2, R12).
+ *  - Errors: arguments are validated in the order NULL -> SHAPE -> ALIGN ->
+ *    SCALE -> RANGE -> DEVICE before anything is enqueued; on error nothing
+ *    is launched and the status is returned (detail: mkq_last_error()).  The
+ *    only device accepted is compute capability 10.0 (B200, sm_100a); there
+ *    is no fallback of any kind.
+ *  - Calls are thread-safe; mkq_last_error() is thread-local.
+ */
+#ifndef MKQ_H
+#define MKQ_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define MKQ_API __attribute__((visibility("default")))
+#else
+#define MKQ_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    MKQ_OK = 0,
+    MKQ_ERR_NULL = 1,      /* a required pointer is NULL                         */
+    MKQ_ERR_SHAPE = 2,     /* dimension out of range / not a multiple required   */
+    MKQ_ERR_ALIGN = 3,     /* pointer or leading dimension misaligned            */
+    MKQ_ERR_SCALE = 4,     /* scale <= 0 or not finite (S:136 reading, R14)      */
+    MKQ_ERR_RANGE = 5,     /* qmin/qmax/bits/mode not representable / unknown    */
+    MKQ_ERR_DEVICE = 6,    /* current device is not compute capability 10.0      */
+    MKQ_ERR_WORKSPACE = 7, /* workspace too small                                */
+    MKQ_ERR_CUDA = 8       /* a CUDA runtime/driver call failed                  */
+} mkq_status;
+
+/* Largest reduction length: the tensor-core accumulator holds 256*sum(a*w)
+ * for int4 operands (see mkq_gemm_w4a4) and |a*w| <= 2^14 for int8, so
+ * K * 2^14 < 2^31 keeps every int32 accumulator exact. */
+#define MKQ_MAX_K 131040
+
+MKQ_API const char *mkq_status_string(int status);
+MKQ_API const char *mkq_last_error(void);     /* thread-local detail of the last error */
+MKQ_API int mkq_version(void);                /* 10000*major + 100*minor + patch        */
+
+/* Epilogue output modes (§8a-a4..a6; R11). */
+typedef enum {
+    MKQ_OUT_F32 = 0,   /* fp32 y = dequant [+GELU]                               */
+    MKQ_OUT_BF16 = 1,  /* bf16, round-to-nearest-even of the fp32 value          */
+    MKQ_OUT_I32 = 2,   /* raw exact int32 accumulators sum_k a*w (no dequant)    */
+    MKQ_OUT_I4 = 3,    /* requantized int4 codes (packed, D2) with s_out (a6)    */
+    MKQ_OUT_I8 = 4,    /* requantized int8 codes with s_out (a6)                 */
+    MKQ_OUT_F16 = 5    /* fp16, round-to-nearest-even of the fp32 value          */
+} mkq_out;
+
+/* Fused epilogue description [host].  For each output (m, n):
+ *   acc  = sum_k a[m,k] * w[n,k]                         (exact int32)
+ *   sc   = fl32(s_a * s_w[n])
+ *   y    = bias ? fmaf((float)acc, sc, bias[n]) : fl32((float)acc * sc)     (R4)
+ *   y    = gelu ? gelu_pinned(y) : y                      (P:98 GELU; R7)
+ *   out  = mode F32/BF16/F16: y;  I4/I8: clamp(rint_even(y / s_out), qmin_out,
+ *          qmax_out)                                      (Eq.1; R1-R3)
+ * A NULL epilogue pointer means {MKQ_OUT_F32, gelu 0}. */
+typedef struct {
+    int32_t out;       /* mkq_out                                          */
+    int32_t gelu;      /* 0 or 1; ignored for MKQ_OUT_I32                  */
+    float s_out;       /* requantization scale (I4/I8 only), > 0, finite   */
+    int32_t qmin_out;  /* requantization code range (I4/I8 only)           */
+    int32_t qmax_out;
+} mkq_epilogue;
+
+/* ------------------------------------------------------------------------
+ * §8a-a1: activation (or weight) quantize + pack, Eq.1:
+ *   q[r, c] = clamp(rint_even(x[r, c] / s), qmin, qmax),  s = scale[0]
+ *   (per_row = 0, per-tensor) or scale[r] (per_row = 1, "per-row").
+ * x      [device] fp32 [rows, cols], row stride ldx_elems (>= cols).
+ * scale  [device] fp32, 1 value or `rows` values.  Values are NOT inspected
+ *        on the host (device memory); they must be > 0 and finite.
+ * bits   4 -> q is packed int4 [rows, cols/2] (cols even); 8 -> int8.
+ * qmin/qmax: code range; int4 within [-8, 7], int8 within [-128, 127],
+ *        qmin < qmax (e.g. activations [-8,7], weights [-7,7]; R1).
+ * q      [device] codes, row stride ldq_bytes (>= packed row bytes).
+ * rows == 0 or cols == 0 is a valid no-op.
+ * ---------------------------------------------------------------------- */
+MKQ_API mkq_status mkq_quantize_pack(const float *x, int64_t rows, int64_t cols, int64_t ldx_elems,
+                             const float *scale, int per_row, int bits, int qmin, int qmax,
+                             void *q, int64_t ldq_bytes, void *stream);
+
+/* §8a-a0: max-abs scale ("maximum of the absolute value", normalised by
+ * l_max, R6; floor 1e-8):  s = max(max|x| / l_max, 1e-8) per row (per_row=1,
+ * s_out[rows]) or per tensor (per_row=0, s_out[1]).  x [device] fp32. */
+MKQ_API mkq_status mkq_absmax_scale(const float *x, int64_t rows, int64_t cols, int64_t ldx_elems,
+                            int per_row, float l_max, float *s_out, void *stream);
+
+/* ------------------------------------------------------------------------
+ * §8a-a2..a6: W4A4 quantized linear layer  out = epi(A W^T).
+ * a   [device] packed int4 activation codes [M, K/2], row stride lda_bytes.
+ * w   [device] packed int4 weight codes [N, K/2] (one row per output
+ *     channel, K-major), row stride ldw_bytes.
+ * s_a per-tensor activation scale (> 0, finite).
+ * s_w [device] fp32 [N] per-output-channel weight scales.
+ * bias[device] fp32 [N] or NULL.
+ * out [device] output [M, N] in the epilogue's mode, row stride ldo_bytes
+ *     (I4: packed [M, N/2]).
+ * Shape rules: M >= 0 (0 = no-op); N % 32 == 0; K % 32 == 0, 32 <= K <=
+ * MKQ_MAX_K.  Alignment: a, w, out 16-byte aligned; lda/ldw/ldo multiples of
+ * 16 bytes and >= the packed row size.  Every code of a and w must be a valid
+ * int4 (any nibble is); results are exact (the GPU accumulates 256*sum(a*w)
+ * in int32 and shifts right by 8).
+ * ws/ws_bytes: workspace, may be NULL/0 when mkq_gemm_workspace_size() == 0.
+ * ---------------------------------------------------------------------- */
+MKQ_API mkq_status mkq_gemm_w4a4(const void *a, int64_t lda_bytes, const void *w, int64_t ldw_bytes,
+                         int64_t M, int64_t N, int64_t K, float s_a, const float *s_w,
+                         const float *bias, const mkq_epilogue *epi, void *out,
+                         int64_t ldo_bytes, void *ws, size_t ws_bytes, void *stream);
+
+/* §8a-a7: W8A8 variant for the paper's mixed 4/8-bit layers:
+ * identical contract with int8 codes a [M, K], w [N, K] (K % 32 == 0). */
+MKQ_API mkq_status mkq_gemm_w8a8(const void *a, int64_t lda_bytes, const void *w, int64_t ldw_bytes,
+                         int64_t M, int64_t N, int64_t K, float s_a, const float *s_w,
+                         const float *bias, const mkq_epilogue *epi, void *out,
+                         int64_t ldo_bytes, void *ws, size_t ws_bytes, void *stream);
+
+MKQ_API size_t mkq_gemm_workspace_size(int64_t M, int64_t N, int64_t K);
+
+/* ------------------------------------------------------------------------
+ * §8a-a8 glue (★s): multi-head self-attention core, Eq.3-5 (with
+ * the q.v^T typo read as q.k^T, R8):  OA = softmax(q k^T / sqrt(d_k)) v,
+ * per sequence and head; softmax in fp32.
+ * qkv  [device] fp16 [tokens, 3*heads*head_dim] = [q | k | v], head a at
+ *      columns a*head_dim of each block; row stride ld_qkv_elems.
+ * cu_seqlens [device] int32 [batch+1] prefix sums of sequence lengths
+ *      (packed "valid tokens", R13) or NULL = `batch` sequences of
+ *      `seq` tokens.  max_seq bounds every length (<= 1024).
+ * out_mode MKQ_OUT_F32 (fp32 OA [tokens, heads*head_dim]) or MKQ_OUT_I4 /
+ *      MKQ_OUT_I8 (OA quantized with s_out, fused; packed like mkq_quantize_pack).
+ * head_dim must be 64.
+ * ---------------------------------------------------------------------- */
+MKQ_API mkq_status mkq_attention(const void *qkv, int64_t ld_qkv_elems, int64_t batch, int64_t max_seq,
+                         const int32_t *cu_seqlens, int64_t tokens, int heads, int head_dim,
+                         int out_mode, float s_out, int qmin, int qmax, void *out,
+                         int64_t ldo_bytes, void *stream);
+
+/* §8a-a8 glue: y = LayerNorm(x + res) * g + b (post-LN, eps, fp32; R9), and
+ * optionally (bits = 4 or 8, else 0) the fused Eq.1 quantize of y with the
+ * per-tensor scale s_q into q (packed like mkq_quantize_pack).
+ * x, res, y [device] fp32 [rows, cols] (row strides ld_elems); res may be
+ * NULL; g, b [device] fp32 [cols]; cols % 4 == 0, cols <= 8192. */
+MKQ_API mkq_status mkq_residual_layernorm(const float *x, const float *res, int64_t rows, int64_t cols,
+                                  int64_t ld_elems, const float *g, const float *b, float eps,
+                                  float *y, int bits, float s_q, int qmin, int qmax, void *q,
+                                  int64_t ldq_bytes, void *stream);
+
+/* ------------------------------------------------------------------------
+ * One quantized post-LN BERT encoder layer (§8a rows a1-a8 composed):
+ *   c   = Q(h; s_qkv_in)                                   a1
+ *   qkv = f16( Linear_{W^{QKV}}(c) )                        a2-a4
+ *   OA  = Attention(qkv) -> Q(.; s_o_in)                    a8 (fused quantize)
+ *   o   = Linear_{W^A}(.) (+b^A), fp32                      a2-a4
+ *   h1  = LN1(o + h) -> fp32 and Q(h1; s_ffn1_in)           a8 + a1 fused
+ *   a2  = Q(GELU(Linear_{W^1}(.)); s_ffn2_in)               a2-a6 (fused)
+ *   f   = Linear_{W^2}(a2), fp32                            a2-a4
+ *   out = LN2(f + h1)                                        a8
+ * bits = 4 (W4A4: every GEMM mkq_gemm_w4a4, codes [-8,7], weights packed
+ * int4) or 8 (W8A8: mkq_gemm_w8a8, codes [-128,127], weights int8).
+ * Weights [device] are [N, K] K-major: W^{QKV} [3h, h], W^A [h, h],
+ * W^1 [ffn, h], W^2 [h, ffn]; row stride = K*bits/8 bytes.
+ * hidden % 64 == 0 (heads*64 == hidden), ffn % 32 == 0.
+ * ---------------------------------------------------------------------- */
+typedef struct {
+    int32_t hidden, heads, ffn, bits;
+    const void *w_qkv, *w_o, *w_1, *w_2;
+    const float *sw_qkv, *sw_o, *sw_1, *sw_2;
+    const float *b_qkv, *b_o, *b_1, *b_2;
+    const float *ln1_g, *ln1_b, *ln2_g, *ln2_b;
+    float s_qkv_in, s_o_in, s_ffn1_in, s_ffn2_in;
+    float ln_eps;
+} mkq_layer;
+
+/* Workspace bytes for `tokens` rows (intermediates of one layer). */
+MKQ_API size_t mkq_bert_layer_workspace_size(const mkq_layer *L, int64_t tokens);
+
+/* h_in, h_out [device] fp32 [tokens, hidden] (may alias: in-place is
+ * allowed).  cu_seqlens as for mkq_attention (NULL = batch x seq; then
+ * tokens must equal batch*seq). */
+MKQ_API mkq_status mkq_bert_layer(const mkq_layer *L, const float *h_in, int64_t batch, int64_t max_seq,
+                          const int32_t *cu_seqlens, int64_t tokens, float *h_out, void *ws,
+                          size_t ws_bytes, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MKQ_H */

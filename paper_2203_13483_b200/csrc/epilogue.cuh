@@ -1,0 +1,89 @@
+// epilogue.cuh -- per-element arithmetic of the fused GEMM epilogue (§8a rows
+// a4 dequant, a5 GELU, a6 requantize) and of the activation quantizer (a1).
+//
+// Every sequence below is pinned by a DESIGN.md reading so that the CUDA
+// path and the CPU oracle compute the same binary32 values:
+//   R2/R3  quantize : q = clamp(rint_even(x / s)), one IEEE division
+//   R4     dequant  : sc = fl(s_a*s_w[n]); y = fma((float)acc, sc, b[n])
+//   R7     gelu     : 0.5*y*(1+erf_pinned(|y|/sqrt2)) with the frozen erf
+//                     polynomial (hex-exact binary32 constants, R7)
+//   R11    bf16/f16 : round-to-nearest-even of the fp32 value
+// Explicit __f*_rn intrinsics keep nvcc from contracting or reordering.
+#pragma once
+#include <cstdint>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+namespace mkq {
+
+// Eq.1: clamp(round(x/s)), ties to even, fp32 division.
+__device__ __forceinline__ int quant_code(float x, float s, int qmin, int qmax) {
+    int q = __float2int_rn(__fdiv_rn(x, s));
+    return min(max(q, qmin), qmax);
+}
+
+// Dequant (P:66 s*q, P:93/P:98 bias; reading R4).
+__device__ __forceinline__ float dequant(int32_t acc, float sc, float b, bool has_bias) {
+    float a = __int2float_rn(acc);
+    return has_bias ? __fmaf_rn(a, sc, b) : __fmul_rn(a, sc);
+}
+
+// gelu_pinned (P:98 GELU, computed in float32 per P:234; reading R7).
+// erf piece 1 (t < 1): t * P(t^2), P degree 6; piece 2 (1 <= t < 3.92):
+// 1 - Q(t - 2.5), Q degree 12; t >= 3.92: 1.  Both pieces are evaluated
+// and selected (branch-free across a warp).
+__device__ __forceinline__ float gelu_pinned(float y) {
+    const float t = __fmul_rn(fabsf(y), 0x1.6a09e6p-1f);
+    const float u1 = __fmul_rn(t, t);
+    float p = 0x1.4fd528p-14f;
+    p = __fmaf_rn(p, u1, -0x1.a63f9ep-11f);
+    p = __fmaf_rn(p, u1, 0x1.545360p-8f);
+    p = __fmaf_rn(p, u1, -0x1.b80286p-6f);
+    p = __fmaf_rn(p, u1, 0x1.ce2d7cp-4f);
+    p = __fmaf_rn(p, u1, -0x1.812740p-2f);
+    p = __fmaf_rn(p, u1, 0x1.20dd76p+0f);
+    const float e1 = __fmul_rn(t, p);
+    const float u2 = __fsub_rn(t, 2.5f);
+    float q = 0x1.3db5fep-17f;
+    q = __fmaf_rn(q, u2, -0x1.5d0ec2p-16f);
+    q = __fmaf_rn(q, u2, -0x1.0bd2eep-14f);
+    q = __fmaf_rn(q, u2, 0x1.23355ep-12f);
+    q = __fmaf_rn(q, u2, -0x1.280846p-12f);
+    q = __fmaf_rn(q, u2, -0x1.29eb5ap-11f);
+    q = __fmaf_rn(q, u2, 0x1.70d992p-9f);
+    q = __fmaf_rn(q, u2, -0x1.901754p-8f);
+    q = __fmaf_rn(q, u2, 0x1.1a5d5cp-7f);
+    q = __fmaf_rn(q, u2, -0x1.11b3b0p-7f);
+    q = __fmaf_rn(q, u2, 0x1.64ef0ap-8f);
+    q = __fmaf_rn(q, u2, -0x1.1d7db8p-9f);
+    q = __fmaf_rn(q, u2, 0x1.aab4b4p-12f);
+    const float e2 = __fsub_rn(1.0f, q);
+    float e = (t < 1.0f) ? e1 : ((t < 3.92f) ? e2 : 1.0f);
+    e = (y < 0.0f) ? -e : e;
+    const float h = __fmul_rn(0.5f, y);
+    return __fmaf_rn(h, e, h);
+}
+
+__device__ __forceinline__ uint32_t pack_nib8(const int (&q)[8]) {
+    uint32_t w = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) w |= (uint32_t)(q[i] & 0xF) << (4 * i);
+    return w;
+}
+
+__device__ __forceinline__ uint32_t pack_byte4(int a, int b, int c, int d) {
+    return (uint32_t)(a & 0xFF) | ((uint32_t)(b & 0xFF) << 8) | ((uint32_t)(c & 0xFF) << 16) |
+           ((uint32_t)(d & 0xFF) << 24);
+}
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
+    __nv_bfloat16 x = __float2bfloat16_rn(a), y = __float2bfloat16_rn(b);
+    return (uint32_t)__bfloat16_as_ushort(x) | ((uint32_t)__bfloat16_as_ushort(y) << 16);
+}
+
+__device__ __forceinline__ uint32_t pack_f16x2(float a, float b) {
+    __half x = __float2half_rn(a), y = __float2half_rn(b);
+    return (uint32_t)__half_as_ushort(x) | ((uint32_t)__half_as_ushort(y) << 16);
+}
+
+}  // namespace mkq

@@ -1,0 +1,326 @@
+// gemm_sm100.cuh -- W4A4 / W8A8 GEMM with exact int32 accumulation on the
+// sm_100a 5th-generation tensor cores (tcgen05.mma kind::i8, D in TMEM) and a
+// fused dequant / GELU / requantize epilogue.  §8(a) rows a2-a7.
+//
+//   out[m, n] = epi( sum_k a[m, k] * w[n, k] )
+//
+// Operands are K-major ("TN"): A [M, K] activations, W [N, K] weights.
+//
+// W4A4 (kInt4): packed int4 tiles (two codes per byte, D2 layout) are
+// TMA-loaded into a staging ring; four "unpack" warps expand them to int8 in
+// the UMMA canonical K-major SWIZZLE_128B layout.  Blackwell has no integer
+// int4 MMA; the unpack keeps the products exact (e2m1 FP4 cannot represent
+// +-5, +-7, -8).  The expansion costs 3 ALU ops per 8 codes:
+//     lo = (p << 4) & 0xF0F0F0F0     -> bytes 16*code[even k]
+//     hi =  p       & 0xF0F0F0F0     -> bytes 16*code[odd  k]
+// i.e. each int8 lane holds 16x the code (no sign-fix needed: the nibble
+// already sits in the top half of the byte) and the K order inside a 32-byte
+// MMA K-step is permuted identically for A and W.  Both operands carry the
+// factor 16, so the s32 accumulator equals 256 * sum_k a*w exactly
+// (|acc| <= 256*64*K < 2^31 for K <= 131040) and the epilogue recovers the
+// true sum with an exact arithmetic shift (acc >> 8).
+//
+// W8A8: int8 tiles are TMA-loaded directly in the SWIZZLE_128B layout.
+//
+// Roles (one CTA per SM, persistent over output tiles):
+//   warp 0      TMA producer (one elected lane)
+//   warp 1      MMA issuer (one lane): 4 x tcgen05.mma (K=32 each) per 128-K block
+//   warp 2      TMEM allocator
+//   warps 4-7   epilogue: tcgen05.ld 32x32b -> dequant/GELU/requant -> global
+//   warps 8-11  int4 -> int8 unpack (W4A4 only)
+// Pipelines: packed ring (TMA -> unpack), int8 ring (unpack|TMA -> MMA),
+// double-buffered TMEM accumulators (MMA -> epilogue), so the epilogue of
+// tile i overlaps the mainloop of tile i+1.
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include "epilogue.cuh"
+#include "ptx.cuh"
+
+namespace mkq {
+
+enum OutMode : int { OUT_F32 = 0, OUT_BF16 = 1, OUT_I32 = 2, OUT_I4 = 3, OUT_I8 = 4, OUT_F16 = 5 };
+
+struct EpiParams {
+    int mode;
+    int gelu;
+    float s_a;
+    const float* s_w;
+    const float* bias;
+    float s_out;
+    int qmin, qmax;
+    void* out;
+    int64_t ldo_bytes;
+};
+
+template <int BN_, bool kInt4_>
+struct GemmCfg {
+    static constexpr int BM = 128;
+    static constexpr int BN = BN_;
+    static constexpr bool kInt4 = kInt4_;
+    static constexpr int BK = 128;                  // K elements per block (=128 int8 bytes/row)
+    static constexpr int kA8 = BM * BK;             // int8 bytes of A per stage
+    static constexpr int kB8 = BN * BK;
+    static constexpr int kStage8 = kA8 + kB8;
+    static constexpr int kAP = BM * BK / 2;         // packed bytes of A per stage
+    static constexpr int kBP = BN * BK / 2;
+    static constexpr int kStageP = kAP + kBP;
+    static constexpr int S8 = kInt4 ? (BN == 256 ? 3 : 4) : 4;
+    static constexpr int SP = kInt4 ? (BN == 256 ? 3 : 4) : 0;
+    static constexpr int kThreads = kInt4 ? 384 : 256;
+    static constexpr uint32_t kTmemCols = 2 * BN;   // double-buffered accumulator
+    static constexpr int kBarBytes = 8 * (2 * S8 + 2 * SP + 4) + 16;
+    static constexpr int kSmem = 1024 + S8 * kStage8 + SP * kStageP + kBarBytes;
+    static_assert(kSmem <= 232448, "shared memory budget");
+};
+
+// ------------------------------------------------------------------ epilogue store
+template <bool kInt4>
+__device__ __forceinline__ void epilogue_store(const EpiParams& ep, const uint32_t (&v)[32],
+                                               int row, int n) {
+    int32_t acc[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) acc[i] = kInt4 ? ((int32_t)v[i] >> 8) : (int32_t)v[i];
+    uint8_t* orow = reinterpret_cast<uint8_t*>(ep.out) + (int64_t)row * ep.ldo_bytes;
+    if (ep.mode == OUT_I32) {
+        int4* o = reinterpret_cast<int4*>(orow + (int64_t)n * 4);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i] = make_int4(acc[4 * i], acc[4 * i + 1], acc[4 * i + 2], acc[4 * i + 3]);
+        return;
+    }
+    float y[32];
+    const bool hb = ep.bias != nullptr;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+        const float sc = __fmul_rn(ep.s_a, __ldg(ep.s_w + n + i));
+        const float b = hb ? __ldg(ep.bias + n + i) : 0.0f;
+        y[i] = dequant(acc[i], sc, b, hb);
+    }
+    if (ep.gelu) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) y[i] = gelu_pinned(y[i]);
+    }
+    switch (ep.mode) {
+    case OUT_F32: {
+        float4* o = reinterpret_cast<float4*>(orow + (int64_t)n * 4);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i] = make_float4(y[4 * i], y[4 * i + 1], y[4 * i + 2], y[4 * i + 3]);
+        break;
+    }
+    case OUT_BF16:
+    case OUT_F16: {
+        uint32_t w[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+            w[i] = ep.mode == OUT_BF16 ? pack_bf16x2(y[2 * i], y[2 * i + 1]) : pack_f16x2(y[2 * i], y[2 * i + 1]);
+        uint4* o = reinterpret_cast<uint4*>(orow + (int64_t)n * 2);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) o[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+        break;
+    }
+    case OUT_I4: {
+        uint32_t w[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            int q[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) q[j] = quant_code(y[8 * i + j], ep.s_out, ep.qmin, ep.qmax);
+            w[i] = pack_nib8(q);
+        }
+        *reinterpret_cast<uint4*>(orow + n / 2) = make_uint4(w[0], w[1], w[2], w[3]);
+        break;
+    }
+    case OUT_I8: {
+        uint32_t w[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            w[i] = pack_byte4(quant_code(y[4 * i], ep.s_out, ep.qmin, ep.qmax),
+                              quant_code(y[4 * i + 1], ep.s_out, ep.qmin, ep.qmax),
+                              quant_code(y[4 * i + 2], ep.s_out, ep.qmin, ep.qmax),
+                              quant_code(y[4 * i + 3], ep.s_out, ep.qmin, ep.qmax));
+        uint4* o = reinterpret_cast<uint4*>(orow + n);
+        o[0] = make_uint4(w[0], w[1], w[2], w[3]);
+        o[1] = make_uint4(w[4], w[5], w[6], w[7]);
+        break;
+    }
+    default:
+        break;
+    }
+}
+
+// ------------------------------------------------------------------ kernel
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::kThreads, 1)
+    gemm_i8tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const EpiParams ep, int M, int N, int K) {
+    constexpr int BM = Cfg::BM, BN = Cfg::BN, S8 = Cfg::S8, SP = Cfg::SP;
+    constexpr bool kInt4 = Cfg::kInt4;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* ring8 = smem;
+    uint8_t* ringP = smem + S8 * Cfg::kStage8;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(ringP + SP * Cfg::kStageP);
+    uint64_t* full8 = bars;
+    uint64_t* empty8 = full8 + S8;
+    uint64_t* fullP = empty8 + S8;
+    uint64_t* emptyP = fullP + SP;
+    uint64_t* tfull = emptyP + SP;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int m_tiles = (M + BM - 1) / BM;
+    const int n_tiles = (N + BN - 1) / BN;
+    const int num_tiles = m_tiles * n_tiles;
+    const int nk = (K + Cfg::BK - 1) / Cfg::BK;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < S8; ++i) {
+            ptx::mbar_init(&full8[i], kInt4 ? 128 : 1);
+            ptx::mbar_init(&empty8[i], 1);
+        }
+        for (int i = 0; i < SP; ++i) {
+            ptx::mbar_init(&fullP[i], 1);
+            ptx::mbar_init(&emptyP[i], 128);
+        }
+        for (int i = 0; i < 2; ++i) {
+            ptx::mbar_init(&tfull[i], 1);
+            ptx::mbar_init(&tempty[i], 128);
+        }
+        ptx::fence_barrier_init();
+    }
+    if (warp == 0 && lane == 0) {
+        ptx::tma_prefetch_desc(&tmA);
+        ptx::tma_prefetch_desc(&tmB);
+    }
+    if (warp == 2) ptx::tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ---------------------------------------------------- TMA producer
+        if (lane == 0) {
+            int s = 0;
+            uint32_t ph = 0;
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+                const int m0 = (tile / n_tiles) * BM, n0 = (tile % n_tiles) * BN;
+                for (int kb = 0; kb < nk; ++kb) {
+                    if constexpr (kInt4) {
+                        ptx::mbar_wait(&emptyP[s], ph ^ 1);
+                        uint8_t* dst = ringP + s * Cfg::kStageP;
+                        ptx::mbar_arrive_expect_tx(&fullP[s], Cfg::kStageP);
+                        ptx::tma_load_2d(&tmA, &fullP[s], dst, kb * (Cfg::BK / 2), m0);
+                        ptx::tma_load_2d(&tmB, &fullP[s], dst + Cfg::kAP, kb * (Cfg::BK / 2), n0);
+                        if (++s == SP) { s = 0; ph ^= 1; }
+                    } else {
+                        ptx::mbar_wait(&empty8[s], ph ^ 1);
+                        uint8_t* dst = ring8 + s * Cfg::kStage8;
+                        ptx::mbar_arrive_expect_tx(&full8[s], Cfg::kStage8);
+                        ptx::tma_load_2d(&tmA, &full8[s], dst, kb * Cfg::BK, m0);
+                        ptx::tma_load_2d(&tmB, &full8[s], dst + Cfg::kA8, kb * Cfg::BK, n0);
+                        if (++s == S8) { s = 0; ph ^= 1; }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------------------------------------------- MMA issuer
+        if (lane == 0) {
+            constexpr uint32_t idesc = ptx::idesc_i8(BM, BN);
+            int s = 0;
+            uint32_t ph = 0;
+            int it = 0;
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+                const int ab = it & 1;
+                const uint32_t aph = (it >> 1) & 1;
+                ptx::mbar_wait(&tempty[ab], aph ^ 1);
+                ptx::tc_fence_after();
+                const uint32_t d = tmem_base + ab * BN;
+                for (int kb = 0; kb < nk; ++kb) {
+                    ptx::mbar_wait(&full8[s], ph);
+                    ptx::tc_fence_after();
+                    const uint32_t a_addr = ptx::smem_u32(ring8 + s * Cfg::kStage8);
+                    const uint32_t b_addr = a_addr + Cfg::kA8;
+#pragma unroll
+                    for (int k = 0; k < Cfg::BK / 32; ++k)
+                        ptx::mma_i8_ss(d, ptx::desc_sw128_kmajor(a_addr + 32 * k),
+                                       ptx::desc_sw128_kmajor(b_addr + 32 * k), idesc,
+                                       (kb | k) != 0);
+                    ptx::mma_commit(&empty8[s]);
+                    if (++s == S8) { s = 0; ph ^= 1; }
+                }
+                ptx::mma_commit(&tfull[ab]);
+            }
+        }
+    } else if (warp >= 4 && warp < 8) {
+        // ---------------------------------------------------- epilogue
+        const int q = warp & 3;   // TMEM lane quadrant owned by this warp
+        int it = 0;
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+            const int m0 = (tile / n_tiles) * BM, n0 = (tile % n_tiles) * BN;
+            const int ab = it & 1;
+            const uint32_t aph = (it >> 1) & 1;
+            ptx::mbar_wait(&tfull[ab], aph);
+            ptx::tc_fence_after();
+            const int row = m0 + q * 32 + lane;
+#pragma unroll 1
+            for (int j = 0; j < BN / 32; ++j) {
+                const int n = n0 + 32 * j;
+                if (n >= N) break;
+                uint32_t v[32];
+                ptx::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + ab * BN + 32 * j, v);
+                ptx::tmem_ld_wait();
+                if (row < M) epilogue_store<kInt4>(ep, v, row, n);
+            }
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(&tempty[ab]);
+        }
+    } else if (kInt4 && warp >= 8) {
+        // ---------------------------------------------------- int4 -> int8 unpack
+        const int u = threadIdx.x - 256;
+        constexpr int kChunks = (BM + BN) * (Cfg::BK / 32);   // 16-byte packed chunks / stage
+        static_assert(kChunks % 128 == 0, "chunk split");
+        int sp = 0, s8 = 0;
+        uint32_t php = 0, ph8 = 0;
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            for (int kb = 0; kb < nk; ++kb) {
+                ptx::mbar_wait(&fullP[sp], php);
+                ptx::mbar_wait(&empty8[s8], ph8 ^ 1);
+                const uint8_t* src = ringP + sp * Cfg::kStageP;
+                uint8_t* dst = ring8 + s8 * Cfg::kStage8;
+#pragma unroll 4
+                for (int i = 0; i < kChunks / 128; ++i) {
+                    const int id = u + 128 * i;
+                    const int r = id >> 2, c = id & 3;
+                    const uint4 p = *reinterpret_cast<const uint4*>(src + r * 64 + c * 16);
+                    uint4 lo, hi;
+                    lo.x = (p.x << 4) & 0xF0F0F0F0u; hi.x = p.x & 0xF0F0F0F0u;
+                    lo.y = (p.y << 4) & 0xF0F0F0F0u; hi.y = p.y & 0xF0F0F0F0u;
+                    lo.z = (p.z << 4) & 0xF0F0F0F0u; hi.z = p.z & 0xF0F0F0F0u;
+                    lo.w = (p.w << 4) & 0xF0F0F0F0u; hi.w = p.w & 0xF0F0F0F0u;
+                    const int r7 = r & 7;
+                    uint8_t* drow = dst + r * 128;
+                    *reinterpret_cast<uint4*>(drow + (((2 * c) ^ r7) << 4)) = lo;
+                    *reinterpret_cast<uint4*>(drow + (((2 * c + 1) ^ r7) << 4)) = hi;
+                }
+                ptx::fence_proxy_async_smem();
+                ptx::mbar_arrive(&full8[s8]);
+                ptx::mbar_arrive(&emptyP[sp]);
+                if (++sp == SP) { sp = 0; php ^= 1; }
+                if (++s8 == S8) { s8 = 0; ph8 ^= 1; }
+            }
+        }
+    }
+
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<Cfg::kTmemCols>(tmem_base);
+    }
+}
+
+}  // namespace mkq

@@ -1,0 +1,88 @@
+// layernorm.cuh -- §8(a) row a8 glue (★s): residual + post-LayerNorm in fp32
+// ("layernorm ... computed using float32"; R9 post-LN, eps 1e-12),
+// optionally fused with the Eq.1 quantize of the normalised row (a1), so the
+// LN output is never re-read from HBM just to be quantized.
+//
+// One warp per row; 128-bit loads; the row stays in registers between the
+// mean pass, the centred-variance pass and the output pass; warp-shuffle
+// reductions.
+#pragma once
+#include <cstdint>
+#include "epilogue.cuh"
+
+namespace mkq {
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+template <int VPL>   // float4 vectors per lane (cols <= 128*VPL)
+__global__ void __launch_bounds__(256) residual_ln_kernel(
+    const float* __restrict__ x, const float* __restrict__ res, int64_t rows, int cols, int64_t ld,
+    const float* __restrict__ g, const float* __restrict__ b, float eps, float* __restrict__ y,
+    int bits, float s_q, int qmin, int qmax, uint8_t* __restrict__ q, int64_t ldq) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int nv = cols >> 2;
+    for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += warps) {
+        const float4* xr = reinterpret_cast<const float4*>(x + r * ld);
+        const float4* rr = res ? reinterpret_cast<const float4*>(res + r * ld) : nullptr;
+        float4 v[VPL];
+        float s = 0.f;
+#pragma unroll
+        for (int i = 0; i < VPL; ++i) {
+            const int c = lane + 32 * i;
+            if (c < nv) {
+                float4 a = __ldcs(xr + c);
+                if (rr) {
+                    const float4 t = __ldcs(rr + c);
+                    a.x += t.x; a.y += t.y; a.z += t.z; a.w += t.w;
+                }
+                v[i] = a;
+                s += (a.x + a.y) + (a.z + a.w);
+            } else {
+                v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        }
+        const float mean = warp_sum(s) / (float)cols;
+        float ss = 0.f;
+#pragma unroll
+        for (int i = 0; i < VPL; ++i) {
+            const int c = lane + 32 * i;
+            if (c < nv) {
+                const float dx = v[i].x - mean, dy = v[i].y - mean, dz = v[i].z - mean, dw = v[i].w - mean;
+                ss += (dx * dx + dy * dy) + (dz * dz + dw * dw);
+            }
+        }
+        const float rstd = rsqrtf(warp_sum(ss) / (float)cols + eps);
+        float4* yr = reinterpret_cast<float4*>(y + r * ld);
+#pragma unroll
+        for (int i = 0; i < VPL; ++i) {
+            const int c = lane + 32 * i;
+            if (c < nv) {
+                const float4 gg = __ldg(reinterpret_cast<const float4*>(g) + c);
+                const float4 bb = __ldg(reinterpret_cast<const float4*>(b) + c);
+                float4 o;
+                o.x = (v[i].x - mean) * rstd * gg.x + bb.x;
+                o.y = (v[i].y - mean) * rstd * gg.y + bb.y;
+                o.z = (v[i].z - mean) * rstd * gg.z + bb.z;
+                o.w = (v[i].w - mean) * rstd * gg.w + bb.w;
+                yr[c] = o;
+                if (bits == 4) {
+                    const int c0 = quant_code(o.x, s_q, qmin, qmax), c1 = quant_code(o.y, s_q, qmin, qmax);
+                    const int c2 = quant_code(o.z, s_q, qmin, qmax), c3 = quant_code(o.w, s_q, qmin, qmax);
+                    const uint16_t w = (uint16_t)((c0 & 0xF) | ((c1 & 0xF) << 4) | ((c2 & 0xF) << 8) | ((c3 & 0xF) << 12));
+                    *reinterpret_cast<uint16_t*>(q + r * ldq + 2 * c) = w;
+                } else if (bits == 8) {
+                    *reinterpret_cast<uint32_t*>(q + r * ldq + 4 * c) =
+                        pack_byte4(quant_code(o.x, s_q, qmin, qmax), quant_code(o.y, s_q, qmin, qmax),
+                                   quant_code(o.z, s_q, qmin, qmax), quant_code(o.w, s_q, qmin, qmax));
+                }
+            }
+        }
+    }
+}
+
+}  // namespace mkq

@@ -1,0 +1,517 @@
+// mkq_abi.cu -- the C ABI of include/mkq.h: argument validation, TMA
+// descriptor encoding/caching, kernel dispatch and the BERT-layer
+// orchestration.  Everything here only enqueues work on the caller's stream.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "../../include/mkq.h"
+#include "attention.cuh"
+#include "gemm_sm100.cuh"
+#include "layernorm.cuh"
+#include "quantize.cuh"
+
+#define MKQ_VERSION 10000
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+mkq_status fail(mkq_status s, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return s;
+}
+
+mkq_status cuda_fail(cudaError_t e, const char* what) {
+    return fail(MKQ_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+bool finite_pos(float s) { return std::isfinite(s) && s > 0.0f; }
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+struct DevInfo {
+    int ok = -1;
+    int sms = 0;
+};
+
+std::mutex g_mu;
+DevInfo g_dev[64];
+
+mkq_status check_device(int* sms = nullptr) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(MKQ_ERR_DEVICE, "no CUDA device: %s", cudaGetErrorString(e));
+    }
+    if (dev < 0 || dev >= 64) return fail(MKQ_ERR_DEVICE, "device ordinal %d", dev);
+    std::lock_guard<std::mutex> lk(g_mu);
+    DevInfo& d = g_dev[dev];
+    if (d.ok < 0) {
+        int maj = 0, min = 0;
+        cudaDeviceGetAttribute(&maj, cudaDevAttrComputeCapabilityMajor, dev);
+        cudaDeviceGetAttribute(&min, cudaDevAttrComputeCapabilityMinor, dev);
+        cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
+        d.ok = (maj == 10 && min == 0) ? 1 : 0;
+        if (!d.ok) snprintf(g_err, sizeof(g_err), "device %d is sm_%d%d, need sm_100 (B200)", dev, maj, min);
+    }
+    if (!d.ok) return MKQ_ERR_DEVICE;
+    if (sms) *sms = d.sms;
+    return MKQ_OK;
+}
+
+// ------------------------------------------------------------------ TMA maps
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    return fn;
+}
+
+using MapKey = std::tuple<uintptr_t, uint64_t, uint64_t, uint64_t, uint32_t, uint32_t, int, int>;
+std::map<MapKey, CUtensorMap> g_maps;
+
+// 2-D uint8 map: inner extent `inner` bytes, `rows` rows, row stride `ld`.
+mkq_status make_map(CUtensorMap* out, const void* base, uint64_t inner, uint64_t rows, uint64_t ld,
+                    uint32_t box_inner, uint32_t box_rows, bool swz128) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    MapKey key{reinterpret_cast<uintptr_t>(base), inner, rows, ld, box_inner, box_rows, swz128 ? 1 : 0, dev};
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        auto it = g_maps.find(key);
+        if (it != g_maps.end()) {
+            *out = it->second;
+            return MKQ_OK;
+        }
+    }
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return fail(MKQ_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[2] = {inner, rows};
+    cuuint64_t strides[1] = {ld};
+    cuuint32_t box[2] = {box_inner, box_rows};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = fn(out, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    swz128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(MKQ_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (g_maps.size() > 4096) g_maps.clear();
+    g_maps[key] = *out;
+    return MKQ_OK;
+}
+
+// ------------------------------------------------------------------ GEMM dispatch
+template <class Cfg>
+mkq_status launch_gemm(const void* a, int64_t lda, const void* w, int64_t ldw, int M, int N, int K,
+                       const mkq::EpiParams& ep, int sms, cudaStream_t st) {
+    static bool attr_set[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!attr_set[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(mkq::gemm_i8tc_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             Cfg::kSmem);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+        attr_set[dev] = true;
+    }
+    CUtensorMap ma, mb;
+    const uint64_t kbytes = Cfg::kInt4 ? (uint64_t)K / 2 : (uint64_t)K;
+    const uint32_t box_in = Cfg::kInt4 ? Cfg::BK / 2 : Cfg::BK;
+    mkq_status s = make_map(&ma, a, kbytes, (uint64_t)M, (uint64_t)lda, box_in, Cfg::BM, !Cfg::kInt4);
+    if (s != MKQ_OK) return s;
+    s = make_map(&mb, w, kbytes, (uint64_t)N, (uint64_t)ldw, box_in, Cfg::BN, !Cfg::kInt4);
+    if (s != MKQ_OK) return s;
+    const int tiles = ((M + Cfg::BM - 1) / Cfg::BM) * ((N + Cfg::BN - 1) / Cfg::BN);
+    const int grid = tiles < sms ? tiles : sms;
+    mkq::gemm_i8tc_kernel<Cfg><<<grid, Cfg::kThreads, Cfg::kSmem, st>>>(ma, mb, ep, M, N, K);
+    cudaError_t e = cudaPeekAtLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "gemm launch");
+    return MKQ_OK;
+}
+
+bool code_range_ok(int bits, int qmin, int qmax) {
+    const int lo = bits == 4 ? -8 : -128, hi = bits == 4 ? 7 : 127;
+    return qmin >= lo && qmax <= hi && qmin < qmax;
+}
+
+mkq_status gemm_common(bool int4, const void* a, int64_t lda, const void* w, int64_t ldw, int64_t M, int64_t N,
+                       int64_t K, float s_a, const float* s_w, const float* bias, const mkq_epilogue* epi, void* out,
+                       int64_t ldo, void* ws, size_t ws_bytes, void* stream) {
+    (void)ws;
+    (void)ws_bytes;
+    mkq_epilogue e{MKQ_OUT_F32, 0, 1.0f, 0, 0};
+    if (epi) e = *epi;
+    if (M < 0 || N < 0 || K < 0) return fail(MKQ_ERR_SHAPE, "negative dimension");
+    if (M == 0) return MKQ_OK;
+    if (!a || !w || !s_w || !out) return fail(MKQ_ERR_NULL, "a, w, s_w and out are required");
+    if (N == 0 || N % 32) return fail(MKQ_ERR_SHAPE, "N=%lld must be a positive multiple of 32", (long long)N);
+    if (K < 32 || K % 32 || K > MKQ_MAX_K)
+        return fail(MKQ_ERR_SHAPE, "K=%lld must be a multiple of 32 in [32, %d]", (long long)K, MKQ_MAX_K);
+    if (M > (1ll << 31) - 256 || N > (1 << 24)) return fail(MKQ_ERR_SHAPE, "M or N too large");
+    const int64_t krow = int4 ? K / 2 : K;
+    int64_t orow;
+    switch (e.out) {
+    case MKQ_OUT_F32: case MKQ_OUT_I32: orow = 4 * N; break;
+    case MKQ_OUT_BF16: case MKQ_OUT_F16: orow = 2 * N; break;
+    case MKQ_OUT_I8: orow = N; break;
+    case MKQ_OUT_I4: orow = N / 2; break;
+    default: return fail(MKQ_ERR_RANGE, "unknown epilogue mode %d", e.out);
+    }
+    if (lda < krow || ldw < krow || ldo < orow) return fail(MKQ_ERR_SHAPE, "leading dimension smaller than a row");
+    if (!aligned16(a) || !aligned16(w) || !aligned16(out) || lda % 16 || ldw % 16 || ldo % 16)
+        return fail(MKQ_ERR_ALIGN, "pointers and leading dimensions must be 16-byte aligned");
+    if (!finite_pos(s_a)) return fail(MKQ_ERR_SCALE, "s_a must be > 0 and finite");
+    const bool requant = e.out == MKQ_OUT_I4 || e.out == MKQ_OUT_I8;
+    if (requant) {
+        if (!finite_pos(e.s_out)) return fail(MKQ_ERR_SCALE, "s_out must be > 0 and finite");
+        if (!code_range_ok(e.out == MKQ_OUT_I4 ? 4 : 8, e.qmin_out, e.qmax_out))
+            return fail(MKQ_ERR_RANGE, "qmin_out/qmax_out not representable");
+    }
+    if (e.gelu != 0 && e.gelu != 1) return fail(MKQ_ERR_RANGE, "gelu must be 0 or 1");
+    int sms = 0;
+    mkq_status s = check_device(&sms);
+    if (s != MKQ_OK) return s;
+
+    mkq::EpiParams ep;
+    ep.mode = e.out;
+    ep.gelu = e.out == MKQ_OUT_I32 ? 0 : e.gelu;
+    ep.s_a = s_a;
+    ep.s_w = s_w;
+    ep.bias = bias;
+    ep.s_out = e.s_out;
+    ep.qmin = e.qmin_out;
+    ep.qmax = e.qmax_out;
+    ep.out = out;
+    ep.ldo_bytes = ldo;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const bool wide = (N % 256 == 0) && (M > 128 * sms / 2 || (M / 128 + 1) * (N / 256) >= sms);
+    if (int4) {
+        if (wide) return launch_gemm<mkq::GemmCfg<256, true>>(a, lda, w, ldw, (int)M, (int)N, (int)K, ep, sms, st);
+        return launch_gemm<mkq::GemmCfg<128, true>>(a, lda, w, ldw, (int)M, (int)N, (int)K, ep, sms, st);
+    }
+    if (wide) return launch_gemm<mkq::GemmCfg<256, false>>(a, lda, w, ldw, (int)M, (int)N, (int)K, ep, sms, st);
+    return launch_gemm<mkq::GemmCfg<128, false>>(a, lda, w, ldw, (int)M, (int)N, (int)K, ep, sms, st);
+}
+
+int grid_for(int64_t work, int threads, int sms) {
+    int64_t g = (work + threads - 1) / threads;
+    const int64_t cap = (int64_t)sms * 16;
+    if (g > cap) g = cap;
+    if (g < 1) g = 1;
+    return (int)g;
+}
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+// Launch the quantize/pack kernels; the scale is a device pointer (scale_dev)
+// or, when that is NULL, the per-tensor value s_val.  Arguments validated.
+mkq_status quantize_internal(const float* x, int64_t rows, int64_t cols, int64_t ldx, const float* scale_dev,
+                             float s_val, int per_row, int bits, int qmin, int qmax, void* q, int64_t ldq, int sms,
+                             cudaStream_t st) {
+    const bool vec = cols % 8 == 0 && ldx % 4 == 0 && aligned16(x) &&
+                     (bits == 4 ? (ldq % 4 == 0 && (reinterpret_cast<uintptr_t>(q) & 3) == 0)
+                                : (ldq % 8 == 0 && (reinterpret_cast<uintptr_t>(q) & 7) == 0));
+    uint8_t* qq = static_cast<uint8_t*>(q);
+    if (vec) {
+        const int g = grid_for(rows * (cols / 8), 256, sms);
+        if (bits == 4) {
+            if (per_row) mkq::quantize_pack_vec_kernel<4, true><<<g, 256, 0, st>>>(x, rows, cols, ldx, scale_dev, s_val, qmin, qmax, qq, ldq);
+            else mkq::quantize_pack_vec_kernel<4, false><<<g, 256, 0, st>>>(x, rows, cols, ldx, scale_dev, s_val, qmin, qmax, qq, ldq);
+        } else {
+            if (per_row) mkq::quantize_pack_vec_kernel<8, true><<<g, 256, 0, st>>>(x, rows, cols, ldx, scale_dev, s_val, qmin, qmax, qq, ldq);
+            else mkq::quantize_pack_vec_kernel<8, false><<<g, 256, 0, st>>>(x, rows, cols, ldx, scale_dev, s_val, qmin, qmax, qq, ldq);
+        }
+    } else {
+        const int g = grid_for(rows * (bits == 4 ? cols / 2 : cols), 256, sms);
+        if (bits == 4) mkq::quantize_pack_any_kernel<4><<<g, 256, 0, st>>>(x, rows, cols, ldx, scale_dev, s_val, per_row, qmin, qmax, qq, ldq);
+        else mkq::quantize_pack_any_kernel<8><<<g, 256, 0, st>>>(x, rows, cols, ldx, scale_dev, s_val, per_row, qmin, qmax, qq, ldq);
+    }
+    cudaError_t e = cudaPeekAtLastError();
+    return e == cudaSuccess ? MKQ_OK : cuda_fail(e, "quantize launch");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* mkq_status_string(int s) {
+    switch (s) {
+    case MKQ_OK: return "MKQ_OK";
+    case MKQ_ERR_NULL: return "MKQ_ERR_NULL";
+    case MKQ_ERR_SHAPE: return "MKQ_ERR_SHAPE";
+    case MKQ_ERR_ALIGN: return "MKQ_ERR_ALIGN";
+    case MKQ_ERR_SCALE: return "MKQ_ERR_SCALE";
+    case MKQ_ERR_RANGE: return "MKQ_ERR_RANGE";
+    case MKQ_ERR_DEVICE: return "MKQ_ERR_DEVICE";
+    case MKQ_ERR_WORKSPACE: return "MKQ_ERR_WORKSPACE";
+    case MKQ_ERR_CUDA: return "MKQ_ERR_CUDA";
+    default: return "MKQ_ERR_UNKNOWN";
+    }
+}
+
+const char* mkq_last_error(void) { return g_err; }
+
+int mkq_version(void) { return MKQ_VERSION; }
+
+mkq_status mkq_quantize_pack(const float* x, int64_t rows, int64_t cols, int64_t ldx, const float* scale,
+                             int per_row, int bits, int qmin, int qmax, void* q, int64_t ldq, void* stream) {
+    if (rows < 0 || cols < 0) return fail(MKQ_ERR_SHAPE, "negative dimension");
+    if (rows == 0 || cols == 0) return MKQ_OK;
+    if (!x || !scale || !q) return fail(MKQ_ERR_NULL, "x, scale and q are required");
+    if (bits != 4 && bits != 8) return fail(MKQ_ERR_RANGE, "bits must be 4 or 8");
+    if (bits == 4 && cols % 2) return fail(MKQ_ERR_SHAPE, "int4 needs an even column count");
+    if (ldx < cols || ldq < (bits == 4 ? cols / 2 : cols)) return fail(MKQ_ERR_SHAPE, "leading dimension too small");
+    if (per_row != 0 && per_row != 1) return fail(MKQ_ERR_RANGE, "per_row must be 0 or 1");
+    if (!code_range_ok(bits, qmin, qmax)) return fail(MKQ_ERR_RANGE, "qmin/qmax not representable in %d bits", bits);
+    int sms = 0;
+    mkq_status s = check_device(&sms);
+    if (s != MKQ_OK) return s;
+    return quantize_internal(x, rows, cols, ldx, scale, 0.0f, per_row, bits, qmin, qmax, q, ldq, sms,
+                             static_cast<cudaStream_t>(stream));
+}
+
+mkq_status mkq_absmax_scale(const float* x, int64_t rows, int64_t cols, int64_t ldx, int per_row, float l_max,
+                            float* s_out, void* stream) {
+    if (rows < 0 || cols < 0) return fail(MKQ_ERR_SHAPE, "negative dimension");
+    if (!x || !s_out) return fail(MKQ_ERR_NULL, "x and s_out are required");
+    if (rows == 0 || cols == 0) return fail(MKQ_ERR_SHAPE, "empty input has no scale");
+    if (ldx < cols) return fail(MKQ_ERR_SHAPE, "leading dimension too small");
+    if (!finite_pos(l_max)) return fail(MKQ_ERR_SCALE, "l_max must be > 0 and finite");
+    if (per_row != 0 && per_row != 1) return fail(MKQ_ERR_RANGE, "per_row must be 0 or 1");
+    int sms = 0;
+    mkq_status s = check_device(&sms);
+    if (s != MKQ_OK) return s;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int vec = (cols % 4 == 0 && ldx % 4 == 0 && aligned16(x)) ? 1 : 0;
+    const int g = grid_for(rows * 32, 256, sms);
+    if (per_row) {
+        mkq::absmax_rows_kernel<<<g, 256, 0, st>>>(x, rows, cols, ldx, vec, l_max, s_out, nullptr);
+    } else {
+        cudaMemsetAsync(s_out, 0, sizeof(float), st);
+        unsigned int* bitsp = reinterpret_cast<unsigned int*>(s_out);
+        mkq::absmax_rows_kernel<<<g, 256, 0, st>>>(x, rows, cols, ldx, vec, l_max, nullptr, bitsp);
+        mkq::absmax_finalize_kernel<<<1, 1, 0, st>>>(bitsp, l_max, s_out);
+    }
+    cudaError_t e = cudaPeekAtLastError();
+    return e == cudaSuccess ? MKQ_OK : cuda_fail(e, "absmax launch");
+}
+
+mkq_status mkq_gemm_w4a4(const void* a, int64_t lda, const void* w, int64_t ldw, int64_t M, int64_t N, int64_t K,
+                         float s_a, const float* s_w, const float* bias, const mkq_epilogue* epi, void* out,
+                         int64_t ldo, void* ws, size_t ws_bytes, void* stream) {
+    return gemm_common(true, a, lda, w, ldw, M, N, K, s_a, s_w, bias, epi, out, ldo, ws, ws_bytes, stream);
+}
+
+mkq_status mkq_gemm_w8a8(const void* a, int64_t lda, const void* w, int64_t ldw, int64_t M, int64_t N, int64_t K,
+                         float s_a, const float* s_w, const float* bias, const mkq_epilogue* epi, void* out,
+                         int64_t ldo, void* ws, size_t ws_bytes, void* stream) {
+    return gemm_common(false, a, lda, w, ldw, M, N, K, s_a, s_w, bias, epi, out, ldo, ws, ws_bytes, stream);
+}
+
+size_t mkq_gemm_workspace_size(int64_t, int64_t, int64_t) { return 0; }
+
+mkq_status mkq_attention(const void* qkv, int64_t ld, int64_t batch, int64_t max_seq, const int32_t* cu,
+                         int64_t tokens, int heads, int head_dim, int out_mode, float s_out, int qmin, int qmax,
+                         void* out, int64_t ldo, void* stream) {
+    if (batch < 0 || max_seq < 0 || tokens < 0) return fail(MKQ_ERR_SHAPE, "negative dimension");
+    if (batch == 0 || tokens == 0) return MKQ_OK;
+    if (!qkv || !out) return fail(MKQ_ERR_NULL, "qkv and out are required");
+    if (head_dim != 64) return fail(MKQ_ERR_SHAPE, "head_dim must be 64");
+    if (heads <= 0 || heads > 65535) return fail(MKQ_ERR_SHAPE, "heads out of range");
+    if (max_seq <= 0 || max_seq > 1024) return fail(MKQ_ERR_SHAPE, "max_seq must be in [1, 1024]");
+    if (batch > 65535) return fail(MKQ_ERR_SHAPE, "batch must be <= 65535");
+    if (!cu && tokens != batch * max_seq) return fail(MKQ_ERR_SHAPE, "tokens != batch*max_seq without cu_seqlens");
+    const int64_t hidden = (int64_t)heads * 64;
+    if (ld < 3 * hidden) return fail(MKQ_ERR_SHAPE, "ld_qkv smaller than 3*hidden");
+    if (!aligned16(qkv) || ld % 8) return fail(MKQ_ERR_ALIGN, "qkv rows must be 16-byte aligned");
+    int64_t orow;
+    if (out_mode == MKQ_OUT_F32) orow = 4 * hidden;
+    else if (out_mode == MKQ_OUT_I4) orow = hidden / 2;
+    else if (out_mode == MKQ_OUT_I8) orow = hidden;
+    else return fail(MKQ_ERR_RANGE, "attention out_mode must be F32, I4 or I8");
+    if (ldo < orow) return fail(MKQ_ERR_SHAPE, "ldo smaller than a row");
+    if (!aligned16(out) || ldo % 16) return fail(MKQ_ERR_ALIGN, "out rows must be 16-byte aligned");
+    if (out_mode != MKQ_OUT_F32) {
+        if (!finite_pos(s_out)) return fail(MKQ_ERR_SCALE, "s_out must be > 0 and finite");
+        if (!code_range_ok(out_mode == MKQ_OUT_I4 ? 4 : 8, qmin, qmax)) return fail(MKQ_ERR_RANGE, "qmin/qmax");
+    }
+    mkq_status s = check_device();
+    if (s != MKQ_OK) return s;
+    mkq::attn::Params p;
+    p.qkv = static_cast<const __half*>(qkv);
+    p.ld = ld;
+    p.cu = cu;
+    p.seq = (int)max_seq;
+    p.hidden = (int)hidden;
+    p.out_mode = out_mode;
+    p.s_out = s_out;
+    p.qmin = qmin;
+    p.qmax = qmax;
+    p.out = out;
+    p.ldo = ldo;
+    dim3 grid((unsigned)((max_seq + 63) / 64), (unsigned)heads, (unsigned)batch);
+    mkq::attn::flash_attn_kernel<<<grid, mkq::attn::kThreads, 0, static_cast<cudaStream_t>(stream)>>>(p);
+    cudaError_t e = cudaPeekAtLastError();
+    return e == cudaSuccess ? MKQ_OK : cuda_fail(e, "attention launch");
+}
+
+mkq_status mkq_residual_layernorm(const float* x, const float* res, int64_t rows, int64_t cols, int64_t ld,
+                                  const float* g, const float* b, float eps, float* y, int bits, float s_q,
+                                  int qmin, int qmax, void* q, int64_t ldq, void* stream) {
+    if (rows < 0 || cols < 0) return fail(MKQ_ERR_SHAPE, "negative dimension");
+    if (rows == 0) return MKQ_OK;
+    if (!x || !g || !b || !y) return fail(MKQ_ERR_NULL, "x, g, b and y are required");
+    if (bits && !q) return fail(MKQ_ERR_NULL, "q is required when bits != 0");
+    if (cols <= 0 || cols % 4 || cols > 8192) return fail(MKQ_ERR_SHAPE, "cols must be a multiple of 4 in [4, 8192]");
+    if (ld < cols || ld % 4) return fail(MKQ_ERR_SHAPE, "ld must be >= cols and a multiple of 4");
+    if (!aligned16(x) || !aligned16(y) || !aligned16(g) || !aligned16(b) || (res && !aligned16(res)))
+        return fail(MKQ_ERR_ALIGN, "x, res, y, g, b must be 16-byte aligned");
+    if (!(eps >= 0.0f) || !std::isfinite(eps)) return fail(MKQ_ERR_SCALE, "eps must be finite and >= 0");
+    if (bits) {
+        if (bits != 4 && bits != 8) return fail(MKQ_ERR_RANGE, "bits must be 0, 4 or 8");
+        if (!finite_pos(s_q)) return fail(MKQ_ERR_SCALE, "s_q must be > 0 and finite");
+        if (!code_range_ok(bits, qmin, qmax)) return fail(MKQ_ERR_RANGE, "qmin/qmax");
+        if (ldq < (bits == 4 ? cols / 2 : cols)) return fail(MKQ_ERR_SHAPE, "ldq too small");
+        if ((reinterpret_cast<uintptr_t>(q) & 3) || ldq % 4) return fail(MKQ_ERR_ALIGN, "q must be 4-byte aligned");
+    }
+    int sms = 0;
+    mkq_status s = check_device(&sms);
+    if (s != MKQ_OK) return s;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int gr = grid_for(rows * 32, 256, sms);
+    uint8_t* qq = static_cast<uint8_t*>(q);
+    const int ci = (int)cols;
+    if (cols <= 1024) mkq::residual_ln_kernel<8><<<gr, 256, 0, st>>>(x, res, rows, ci, ld, g, b, eps, y, bits, s_q, qmin, qmax, qq, ldq);
+    else if (cols <= 2048) mkq::residual_ln_kernel<16><<<gr, 256, 0, st>>>(x, res, rows, ci, ld, g, b, eps, y, bits, s_q, qmin, qmax, qq, ldq);
+    else mkq::residual_ln_kernel<64><<<gr, 256, 0, st>>>(x, res, rows, ci, ld, g, b, eps, y, bits, s_q, qmin, qmax, qq, ldq);
+    cudaError_t e = cudaPeekAtLastError();
+    return e == cudaSuccess ? MKQ_OK : cuda_fail(e, "layernorm launch");
+}
+
+// ------------------------------------------------------------------ BERT layer
+struct LayerWs {
+    size_t codes_in, qkv, codes_oa, o, h1, codes_h1, codes_ffn2, f, total;
+};
+
+static LayerWs layer_ws(const mkq_layer* L, int64_t T) {
+    LayerWs w;
+    const int64_t h = L->hidden, F = L->ffn;
+    const int64_t cb = L->bits == 4 ? 1 : 2;   // code bytes per 2 elements
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off += align256(bytes); return o; };
+    w.codes_in = take((size_t)T * h * cb / 2);
+    w.qkv = take((size_t)T * 3 * h * 2);
+    w.codes_oa = take((size_t)T * h * cb / 2);
+    w.o = take((size_t)T * h * 4);
+    w.h1 = take((size_t)T * h * 4);
+    w.codes_h1 = take((size_t)T * h * cb / 2);
+    w.codes_ffn2 = take((size_t)T * F * cb / 2);
+    w.f = take((size_t)T * h * 4);
+    w.total = off;
+    return w;
+}
+
+size_t mkq_bert_layer_workspace_size(const mkq_layer* L, int64_t tokens) {
+    if (!L || tokens < 0) return 0;
+    return layer_ws(L, tokens).total;
+}
+
+mkq_status mkq_bert_layer(const mkq_layer* L, const float* h_in, int64_t batch, int64_t max_seq,
+                          const int32_t* cu, int64_t T, float* h_out, void* ws, size_t ws_bytes, void* stream) {
+    if (!L) return fail(MKQ_ERR_NULL, "layer description is NULL");
+    if (batch < 0 || max_seq < 0 || T < 0) return fail(MKQ_ERR_SHAPE, "negative dimension");
+    if (T == 0) return MKQ_OK;
+    if (!h_in || !h_out || !ws) return fail(MKQ_ERR_NULL, "h_in, h_out and ws are required");
+    if (!L->w_qkv || !L->w_o || !L->w_1 || !L->w_2 || !L->sw_qkv || !L->sw_o || !L->sw_1 || !L->sw_2 ||
+        !L->ln1_g || !L->ln1_b || !L->ln2_g || !L->ln2_b)
+        return fail(MKQ_ERR_NULL, "layer weights, scales and LN parameters are required");
+    if (L->bits != 4 && L->bits != 8) return fail(MKQ_ERR_RANGE, "bits must be 4 or 8");
+    if (L->hidden <= 0 || L->hidden % 64 || L->heads * 64 != L->hidden)
+        return fail(MKQ_ERR_SHAPE, "hidden must equal heads*64");
+    if (L->ffn <= 0 || L->ffn % 32) return fail(MKQ_ERR_SHAPE, "ffn must be a positive multiple of 32");
+    if (!finite_pos(L->s_qkv_in) || !finite_pos(L->s_o_in) || !finite_pos(L->s_ffn1_in) || !finite_pos(L->s_ffn2_in))
+        return fail(MKQ_ERR_SCALE, "activation scales must be > 0 and finite");
+    if (!cu && T != batch * max_seq) return fail(MKQ_ERR_SHAPE, "tokens != batch*max_seq without cu_seqlens");
+    const LayerWs W = layer_ws(L, T);
+    if (ws_bytes < W.total) return fail(MKQ_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes, W.total);
+    if (!aligned16(ws)) return fail(MKQ_ERR_ALIGN, "workspace must be 16-byte aligned");
+    mkq_status s = check_device();
+    if (s != MKQ_OK) return s;
+
+    const int bits = L->bits;
+    const int qlo = bits == 4 ? -8 : -128, qhi = bits == 4 ? 7 : 127;
+    const int64_t h = L->hidden, F = L->ffn;
+    const int64_t cbh = bits == 4 ? h / 2 : h;   // code bytes per hidden row
+    const int64_t cbf = bits == 4 ? F / 2 : F;
+    uint8_t* base = static_cast<uint8_t*>(ws);
+    uint8_t* codes_in = base + W.codes_in;
+    __half* qkv = reinterpret_cast<__half*>(base + W.qkv);
+    uint8_t* codes_oa = base + W.codes_oa;
+    float* o = reinterpret_cast<float*>(base + W.o);
+    float* h1 = reinterpret_cast<float*>(base + W.h1);
+    uint8_t* codes_h1 = base + W.codes_h1;
+    uint8_t* codes_ffn2 = base + W.codes_ffn2;
+    float* f = reinterpret_cast<float*>(base + W.f);
+    auto gemm = bits == 4 ? mkq_gemm_w4a4 : mkq_gemm_w8a8;
+
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    int sms = 0;
+    check_device(&sms);
+#define MKQ_TRY(x)                       \
+    do {                                 \
+        mkq_status _s = (x);             \
+        if (_s != MKQ_OK) return _s;     \
+    } while (0)
+    // a1: quantize the layer input (per-tensor static scale, by value)
+    MKQ_TRY(quantize_internal(h_in, T, h, h, nullptr, L->s_qkv_in, 0, bits, qlo, qhi, codes_in, cbh, sms, st));
+    // a2-a4: QKV projection -> fp16 q|k|v (R10)
+    mkq_epilogue e_f16{MKQ_OUT_F16, 0, 1.0f, 0, 0};
+    MKQ_TRY(gemm(codes_in, cbh, L->w_qkv, cbh, T, 3 * h, h, L->s_qkv_in, L->sw_qkv, L->b_qkv, &e_f16, qkv,
+                 3 * h * 2, nullptr, 0, stream));
+    // a8: attention core, fused quantize of OA with s_o_in
+    MKQ_TRY(mkq_attention(qkv, 3 * h, batch, max_seq, cu, T, L->heads, 64, bits == 4 ? MKQ_OUT_I4 : MKQ_OUT_I8,
+                          L->s_o_in, qlo, qhi, codes_oa, cbh, stream));
+    // W^A projection (+ b^A) -> fp32
+    mkq_epilogue e_f32{MKQ_OUT_F32, 0, 1.0f, 0, 0};
+    MKQ_TRY(gemm(codes_oa, cbh, L->w_o, cbh, T, h, h, L->s_o_in, L->sw_o, L->b_o, &e_f32, o, h * 4, nullptr, 0,
+                 stream));
+    // LN1(o + h) -> h1 fp32 and its codes for FFN1 (fused a1)
+    MKQ_TRY(mkq_residual_layernorm(o, h_in, T, h, h, L->ln1_g, L->ln1_b, L->ln_eps, h1, bits, L->s_ffn1_in, qlo,
+                                   qhi, codes_h1, cbh, stream));
+    // FFN1: GELU + requantize to the FFN2 input codes (a5, a6 fused)
+    mkq_epilogue e_ffn1{bits == 4 ? MKQ_OUT_I4 : MKQ_OUT_I8, 1, L->s_ffn2_in, qlo, qhi};
+    MKQ_TRY(gemm(codes_h1, cbh, L->w_1, cbh, T, F, h, L->s_ffn1_in, L->sw_1, L->b_1, &e_ffn1, codes_ffn2, cbf,
+                 nullptr, 0, stream));
+    // FFN2 -> fp32
+    MKQ_TRY(gemm(codes_ffn2, cbf, L->w_2, cbf, T, h, F, L->s_ffn2_in, L->sw_2, L->b_2, &e_f32, f, h * 4, nullptr,
+                 0, stream));
+    // LN2(f + h1) -> h_out
+    MKQ_TRY(mkq_residual_layernorm(f, h1, T, h, h, L->ln2_g, L->ln2_b, L->ln_eps, h_out, 0, 1.0f, 0, 0, nullptr,
+                                   0, stream));
+#undef MKQ_TRY
+    return MKQ_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,168 @@
+"""Thin PyTorch binding over the C ABI (include/mkq.h): argument marshalling
+only.  Every function is named after the C entry point it calls; every step
+of the hot path runs in libmkq.so's CUDA kernels.  Tensors must live on a
+CUDA device (a B200); nothing here computes on the host.
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Optional
+
+import torch
+
+from ._lib import (OUT_BF16, OUT_F16, OUT_F32, OUT_I32, OUT_I4, OUT_I8, MkqEpilogue, MkqLayer,
+                   check, lib)
+
+__all__ = ["mkq_quantize_pack", "mkq_absmax_scale", "mkq_gemm_w4a4", "mkq_gemm_w8a8",
+           "mkq_attention", "mkq_residual_layernorm", "mkq_bert_layer", "out_dtype_bytes",
+           "OUT_F32", "OUT_BF16", "OUT_I32", "OUT_I4", "OUT_I8", "OUT_F16"]
+
+
+def _stream(stream: Optional[torch.cuda.Stream]):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("mkq: tensors must be CUDA tensors (no host fallback)")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _row_bytes(t: torch.Tensor) -> int:
+    assert t.dim() == 2 and t.stride(1) == 1, "row-major 2-D tensor with unit column stride required"
+    return t.stride(0) * t.element_size()
+
+
+def out_dtype_bytes(mode: int):
+    return {OUT_F32: (torch.float32, 4), OUT_I32: (torch.int32, 4), OUT_BF16: (torch.bfloat16, 2),
+            OUT_F16: (torch.float16, 2), OUT_I8: (torch.int8, 1), OUT_I4: (torch.uint8, 0.5)}[mode]
+
+
+def mkq_quantize_pack(x: torch.Tensor, scale: torch.Tensor, bits: int = 4, qmin: int = -8, qmax: int = 7,
+                      per_row: bool = False, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """Eq.1 quantize + pack (§8a-a1).  x fp32 [rows, cols]; scale fp32 device
+    tensor with 1 (per-tensor) or rows (per-row) values."""
+    rows, cols = x.shape
+    if out is None:
+        out = torch.empty((rows, cols // 2 if bits == 4 else cols),
+                          dtype=torch.uint8 if bits == 4 else torch.int8, device=x.device)
+    check("mkq_quantize_pack", lib().mkq_quantize_pack(
+        _ptr(x), rows, cols, x.stride(0), _ptr(scale), int(per_row), bits, qmin, qmax, _ptr(out),
+        _row_bytes(out), _stream(stream)))
+    return out
+
+
+def mkq_absmax_scale(x: torch.Tensor, l_max: float, per_row: bool = True, out: Optional[torch.Tensor] = None,
+                     stream=None) -> torch.Tensor:
+    """a0 calibration: s = max(max|x| / l_max, 1e-8) per row or per tensor."""
+    rows, cols = x.shape
+    if out is None:
+        out = torch.empty(rows if per_row else 1, dtype=torch.float32, device=x.device)
+    check("mkq_absmax_scale", lib().mkq_absmax_scale(_ptr(x), rows, cols, x.stride(0), int(per_row),
+                                                     float(l_max), _ptr(out), _stream(stream)))
+    return out
+
+
+def _gemm(name: str, a, w, K: int, s_a: float, s_w, bias, mode: int, gelu: bool, s_out: float, qmin: int,
+          qmax: int, out, stream):
+    M, N = a.shape[0], w.shape[0]
+    if out is None:
+        dt, nb = out_dtype_bytes(mode)
+        out = torch.empty((M, int(N * nb) if mode == OUT_I4 else N), dtype=dt, device=a.device)
+    epi = MkqEpilogue(mode, int(gelu), float(s_out), qmin, qmax)
+    fn = getattr(lib(), name)
+    check(name, fn(_ptr(a), _row_bytes(a), _ptr(w), _row_bytes(w), M, N, K, float(s_a), _ptr(s_w), _ptr(bias),
+                   ctypes.byref(epi), _ptr(out), _row_bytes(out), None, 0, _stream(stream)))
+    return out
+
+
+def mkq_gemm_w4a4(a: torch.Tensor, w: torch.Tensor, s_a: float, s_w: torch.Tensor,
+                  bias: Optional[torch.Tensor] = None, mode: int = OUT_F32, gelu: bool = False,
+                  s_out: float = 1.0, qmin: int = -8, qmax: int = 7, out: Optional[torch.Tensor] = None,
+                  K: Optional[int] = None, stream=None) -> torch.Tensor:
+    """W4A4 linear (§8a-a2..a6): a packed [M, K/2], w packed [N, K/2]."""
+    K = K if K is not None else a.shape[1] * 2
+    return _gemm("mkq_gemm_w4a4", a, w, K, s_a, s_w, bias, mode, gelu, s_out, qmin, qmax, out, stream)
+
+
+def mkq_gemm_w8a8(a: torch.Tensor, w: torch.Tensor, s_a: float, s_w: torch.Tensor,
+                  bias: Optional[torch.Tensor] = None, mode: int = OUT_F32, gelu: bool = False,
+                  s_out: float = 1.0, qmin: int = -128, qmax: int = 127, out: Optional[torch.Tensor] = None,
+                  K: Optional[int] = None, stream=None) -> torch.Tensor:
+    """W8A8 linear (§8a-a7): a int8 [M, K], w int8 [N, K]."""
+    K = K if K is not None else a.shape[1]
+    return _gemm("mkq_gemm_w8a8", a, w, K, s_a, s_w, bias, mode, gelu, s_out, qmin, qmax, out, stream)
+
+
+def mkq_attention(qkv: torch.Tensor, heads: int, batch: int, max_seq: int,
+                  cu_seqlens: Optional[torch.Tensor] = None, mode: int = OUT_F32, s_out: float = 1.0,
+                  qmin: int = -8, qmax: int = 7, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """Attention core (Eq.3-5) on fp16 qkv [tokens, 3*hidden]."""
+    T = qkv.shape[0]
+    hidden = heads * 64
+    if out is None:
+        if mode == OUT_F32:
+            out = torch.empty((T, hidden), dtype=torch.float32, device=qkv.device)
+        elif mode == OUT_I4:
+            out = torch.empty((T, hidden // 2), dtype=torch.uint8, device=qkv.device)
+        else:
+            out = torch.empty((T, hidden), dtype=torch.int8, device=qkv.device)
+    check("mkq_attention", lib().mkq_attention(
+        _ptr(qkv), qkv.stride(0), batch, max_seq, _ptr(cu_seqlens), T, heads, 64, mode, float(s_out), qmin, qmax,
+        _ptr(out), _row_bytes(out), _stream(stream)))
+    return out
+
+
+def mkq_residual_layernorm(x: torch.Tensor, res: Optional[torch.Tensor], g: torch.Tensor, b: torch.Tensor,
+                           eps: float = 1e-12, bits: int = 0, s_q: float = 1.0, qmin: int = -8, qmax: int = 7,
+                           y: Optional[torch.Tensor] = None, q: Optional[torch.Tensor] = None, stream=None):
+    """y = LN(x + res) (post-LN, R9) [+ fused Eq.1 quantize of y]."""
+    rows, cols = x.shape
+    if y is None:
+        y = torch.empty_like(x)
+    if bits and q is None:
+        q = torch.empty((rows, cols // 2 if bits == 4 else cols), dtype=torch.uint8 if bits == 4 else torch.int8,
+                        device=x.device)
+    check("mkq_residual_layernorm", lib().mkq_residual_layernorm(
+        _ptr(x), _ptr(res), rows, cols, x.stride(0), _ptr(g), _ptr(b), float(eps), _ptr(y), bits, float(s_q), qmin,
+        qmax, _ptr(q), _row_bytes(q) if q is not None else 0, _stream(stream)))
+    return (y, q) if bits else y
+
+
+class QLayer:
+    """Device-resident parameters of one quantized BERT layer (mkq_layer)."""
+
+    FIELDS = ("w_qkv", "w_o", "w_1", "w_2", "sw_qkv", "sw_o", "sw_1", "sw_2", "b_qkv", "b_o", "b_1", "b_2",
+              "ln1_g", "ln1_b", "ln2_g", "ln2_b")
+
+    def __init__(self, hidden: int, heads: int, ffn: int, bits: int, tensors: dict, scales: dict,
+                 ln_eps: float = 1e-12):
+        self.hidden, self.heads, self.ffn, self.bits = hidden, heads, ffn, bits
+        self.t = {k: tensors[k].contiguous() for k in self.FIELDS}
+        self.scales = {k: float(scales[k]) for k in ("s_qkv_in", "s_o_in", "s_ffn1_in", "s_ffn2_in")}
+        self.ln_eps = ln_eps
+        self.c = MkqLayer(hidden, heads, ffn, bits, *[self.t[k].data_ptr() for k in self.FIELDS],
+                          self.scales["s_qkv_in"], self.scales["s_o_in"], self.scales["s_ffn1_in"],
+                          self.scales["s_ffn2_in"], float(ln_eps))
+
+    def workspace_size(self, tokens: int) -> int:
+        return int(lib().mkq_bert_layer_workspace_size(ctypes.byref(self.c), tokens))
+
+
+def mkq_bert_layer(layer: QLayer, h_in: torch.Tensor, batch: int, max_seq: int,
+                   cu_seqlens: Optional[torch.Tensor] = None, h_out: Optional[torch.Tensor] = None,
+                   ws: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """One quantized post-LN BERT layer on h_in fp32 [tokens, hidden]."""
+    T = h_in.shape[0]
+    if h_out is None:
+        h_out = torch.empty_like(h_in)
+    need = layer.workspace_size(T)
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(need, dtype=torch.uint8, device=h_in.device)
+    check("mkq_bert_layer", lib().mkq_bert_layer(
+        ctypes.byref(layer.c), _ptr(h_in), batch, max_seq, _ptr(cu_seqlens), T, _ptr(h_out), _ptr(ws), ws.numel(),
+        _stream(stream)))
+    return h_out

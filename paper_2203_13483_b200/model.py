@@ -1,0 +1,124 @@
+"""Layer assembly on top of the C ABI: offline weight prep (§8a-a0), offline
+activation-scale calibration (★s host rule) and the
+mixed-precision stack (P:243 'start from the last layer'; P:46 50% int4 +
+50% int8).  Marshalling only: all arithmetic runs in libmkq.so kernels, except
+the calibration statistic (the 99.99th percentile of |activation|, a host
+rule of the offline calibration step)."""
+from __future__ import annotations
+
+from typing import Dict, List, Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import mkq as M
+
+
+def act_range(bits: int):
+    return (-8, 7) if bits == 4 else (-128, 127)
+
+
+def weight_range(bits: int):
+    return (-7, 7) if bits == 4 else (-127, 127)
+
+
+def prepare_weight(w: torch.Tensor, bits: int):
+    """a0: per-output-channel max-abs scale (R5/R6) and packed codes."""
+    lo, hi = weight_range(bits)
+    s_w = M.mkq_absmax_scale(w, float(hi), per_row=True)
+    q = M.mkq_quantize_pack(w, s_w, bits, lo, hi, per_row=True)
+    return q, s_w
+
+
+def abs_quantile(x: torch.Tensor, p: float = 0.9999) -> np.float32:
+    """Calibration statistic (P:72 'top 0.01% largest value'): sort-based
+    p-quantile of |x| with linear interpolation, fp64, rounded to fp32."""
+    a = np.sort(np.abs(x.detach().double().cpu().numpy()).ravel())
+    pos = p * (a.size - 1)
+    lo = int(np.floor(pos))
+    hi = min(lo + 1, a.size - 1)
+    return np.float32(a[lo] + (pos - lo) * (a[hi] - a[lo]))
+
+
+def act_scale(x: torch.Tensor, l_max: int) -> float:
+    return float(np.float32(abs_quantile(x)) / np.float32(l_max))
+
+
+def build_layer(params, bits: int, device="cuda", scales: Optional[Dict[str, float]] = None,
+                ln_eps: float = 1e-12) -> M.QLayer:
+    """params: synth.LayerFloat-like object with fp32 numpy/torch arrays."""
+    def t(a):
+        return torch.as_tensor(np.ascontiguousarray(a) if isinstance(a, np.ndarray) else a).to(device)
+
+    T = {}
+    for name, wn, bn in (("qkv", "w_qkv", "b_qkv"), ("o", "w_o", "b_o"), ("1", "w_1", "b_1"), ("2", "w_2", "b_2")):
+        q, s = prepare_weight(t(getattr(params, wn)).float(), bits)
+        T["w_" + name] = q
+        T["sw_" + name] = s
+        T["b_" + name] = t(getattr(params, bn)).float()
+    for n in ("ln1_g", "ln1_b", "ln2_g", "ln2_b"):
+        T[n] = t(getattr(params, n)).float()
+    sc = scales or {"s_qkv_in": 1.0, "s_o_in": 1.0, "s_ffn1_in": 1.0, "s_ffn2_in": 1.0}
+    return M.QLayer(params.hidden, params.heads, params.ffn, bits, T, sc, ln_eps)
+
+
+def calibrate(layer: M.QLayer, h: torch.Tensor, batch: int, max_seq: int,
+              cu_seqlens: Optional[torch.Tensor] = None) -> Dict[str, float]:
+    """Sequential calibration of the four static activation scales on a
+    calibration batch, each quantization point in pipeline
+    order with the scales already fixed upstream; returns and installs them."""
+    bits, hd, F = layer.bits, layer.hidden, layer.ffn
+    lo, hi = act_range(bits)
+    t = layer.t
+    gemm = M.mkq_gemm_w4a4 if bits == 4 else M.mkq_gemm_w8a8
+    s = {}
+    s["s_qkv_in"] = act_scale(h, hi)
+    c = M.mkq_quantize_pack(h, torch.tensor([s["s_qkv_in"]], device=h.device), bits, lo, hi)
+    qkv = gemm(c, t["w_qkv"], s["s_qkv_in"], t["sw_qkv"], t["b_qkv"], mode=M.OUT_F16, K=hd)
+    oa = M.mkq_attention(qkv, layer.heads, batch, max_seq, cu_seqlens, mode=M.OUT_F32)
+    s["s_o_in"] = act_scale(oa, hi)
+    c = M.mkq_quantize_pack(oa, torch.tensor([s["s_o_in"]], device=h.device), bits, lo, hi)
+    o = gemm(c, t["w_o"], s["s_o_in"], t["sw_o"], t["b_o"], mode=M.OUT_F32, K=hd)
+    h1 = M.mkq_residual_layernorm(o, h, t["ln1_g"], t["ln1_b"], layer.ln_eps)
+    s["s_ffn1_in"] = act_scale(h1, hi)
+    c = M.mkq_quantize_pack(h1, torch.tensor([s["s_ffn1_in"]], device=h.device), bits, lo, hi)
+    g = gemm(c, t["w_1"], s["s_ffn1_in"], t["sw_1"], t["b_1"], mode=M.OUT_F32, gelu=True, K=hd)
+    s["s_ffn2_in"] = act_scale(g, hi)
+    rebuilt = M.QLayer(hd, layer.heads, F, bits, layer.t, s, layer.ln_eps)
+    layer.__dict__.update(rebuilt.__dict__)
+    return s
+
+
+def bit_plan(layers: int, n_int4: int) -> List[int]:
+    """'we start from the last layer for quantization': the last
+    n_int4 layers are W4A4, the rest W8A8 (Table 1 caption P:211)."""
+    return [4 if i >= layers - n_int4 else 8 for i in range(layers)]
+
+
+def compression_ratio(plan: Sequence[int]) -> float:
+    """fp32 bits / mean weight bits (P:30 '5.3x of bits reduction')."""
+    return 32.0 / (sum(plan) / len(plan))
+
+
+class Encoder:
+    """A stack of quantized BERT layers run back to back through
+    mkq_bert_layer on one stream (CUDA-graph capturable)."""
+
+    def __init__(self, layers: List[M.QLayer]):
+        self.layers = layers
+        self._ws = None
+        self._buf = None
+
+    def __call__(self, h: torch.Tensor, batch: int, max_seq: int, cu_seqlens=None, stream=None,
+                 out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """Runs every layer in place on `out` (a copy of h unless given)."""
+        T = h.shape[0]
+        need = max(l.workspace_size(T) for l in self.layers)
+        if self._ws is None or self._ws.numel() < need or self._ws.device != h.device:
+            self._ws = torch.empty(need, dtype=torch.uint8, device=h.device)
+        cur = h
+        for l in self.layers:
+            cur = M.mkq_bert_layer(l, cur, batch, max_seq, cu_seqlens, h_out=out, ws=self._ws, stream=stream)
+            if out is None:
+                out = cur
+        return cur

@@ -1,0 +1,234 @@
+"""GPU parity of every CUDA entry point against the CPU oracle, through the
+C ABI (paper_2203_13483_b200.mkq -> libmkq.so).  Bit-exact on codes, int32
+accumulators, fp32/fp16/bf16 epilogue outputs (the epilogue pins its fp32
+op order, R4/R7/R11); tolerance only for the fp32 glue (attention,
+LayerNorm) whose fused quantize is still checked bit-exactly against the
+oracle applied to the GPU's own fp32 values (stage-wise replay)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from oracle import layer as OL
+import synth
+
+pytestmark = pytest.mark.gpu
+
+from paper_2203_13483_b200 import mkq as M  # noqa: E402
+
+DEV = "cuda:0"
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+# ------------------------------------------------------------------ a1 quantize
+@pytest.mark.parametrize("rows,cols", [(1, 32), (7, 96), (128, 768), (1000, 1024), (3, 6), (5, 1030)])
+@pytest.mark.parametrize("bits", [4, 8])
+def test_quantize_pack_parity(rows, cols, bits):
+    x = synth.activations(rows, cols, seed=rows * 7 + cols)
+    lo, hi = (-8, 7) if bits == 4 else (-128, 127)
+    s = np.float32(0.5558) if bits == 4 else np.float32(0.0306)
+    q = M.mkq_quantize_pack(dev(x), dev(np.array([s], np.float32)), bits, lo, hi)
+    ref = oracle.quantize(x, s, lo, hi)
+    if bits == 4:
+        assert np.array_equal(host(q), oracle.pack_int4(ref))
+    else:
+        assert np.array_equal(host(q).view(np.int8), ref)
+
+
+def test_quantize_per_row_weights_and_absmax():
+    w = synth.weight(768, 1024, seed=3)
+    s_gpu = M.mkq_absmax_scale(dev(w), 7.0, per_row=True)
+    s_ref = oracle.absmax_scale(w, 7)
+    assert np.array_equal(host(s_gpu), s_ref)
+    q = M.mkq_quantize_pack(dev(w), s_gpu, 4, -7, 7, per_row=True)
+    assert np.array_equal(host(q), oracle.pack_int4(oracle.quantize(w, s_ref, -7, 7, per_row=True)))
+    st = M.mkq_absmax_scale(dev(w), 127.0, per_row=False)
+    assert np.array_equal(host(st), oracle.absmax_scale(w, 127, per_row=False))
+
+
+def test_quantize_ties_half_even():
+    x = ((np.arange(-20, 20, dtype=np.float32) + np.float32(0.5)) * np.float32(0.25))[None, :].repeat(2, 0)
+    q = M.mkq_quantize_pack(dev(x), dev(np.float32([0.25])), 8, -128, 127)
+    assert np.array_equal(host(q).view(np.int8), oracle.quantize(x, np.float32(0.25), -128, 127))
+
+
+# ------------------------------------------------------------------ a2-a7 GEMM
+def _codes(rng, M_, N_, K_, bits):
+    if bits == 4:
+        A = rng.integers(-8, 8, (M_, K_)).astype(np.int8)
+        W = rng.integers(-7, 8, (N_, K_)).astype(np.int8)
+    else:
+        A = rng.integers(-128, 128, (M_, K_)).astype(np.int8)
+        W = rng.integers(-127, 128, (N_, K_)).astype(np.int8)
+    return A, W
+
+
+def _run(bits, A, W, s_a, s_w, b, **kw):
+    K_ = A.shape[1]
+    if bits == 4:
+        return M.mkq_gemm_w4a4(dev(oracle.pack_int4(A)), dev(oracle.pack_int4(W)), s_a, dev(s_w),
+                               None if b is None else dev(b), K=K_, **kw)
+    return M.mkq_gemm_w8a8(dev(A), dev(W), s_a, dev(s_w), None if b is None else dev(b), K=K_, **kw)
+
+
+SHAPES = [(1, 32, 32), (7, 64, 96), (128, 768, 768), (129, 256, 160), (300, 512, 1024), (257, 288, 64),
+          (1000, 3072, 768)]
+
+
+@pytest.mark.parametrize("bits", [4, 8])
+@pytest.mark.parametrize("Mm,N,K", SHAPES)
+def test_gemm_raw_i32_bitexact(bits, Mm, N, K):
+    rng = np.random.default_rng(Mm * 31 + N + K)
+    A, W = _codes(rng, Mm, N, K, bits)
+    out = _run(bits, A, W, 1.0, np.ones(N, np.float32), None, mode=M.OUT_I32)
+    assert np.array_equal(host(out), oracle.gemm_i32(A, W))
+
+
+@pytest.mark.parametrize("bits", [4, 8])
+@pytest.mark.parametrize("mode", [M.OUT_F32, M.OUT_F16, M.OUT_BF16])
+@pytest.mark.parametrize("gelu", [False, True])
+def test_gemm_float_epilogues_bitexact(bits, mode, gelu):
+    rng = np.random.default_rng(17 + mode)
+    Mm, N, K = 300, 768, 1024
+    A, W = _codes(rng, Mm, N, K, bits)
+    s_a = np.float32(0.5558 if bits == 4 else 0.0306)
+    s_w = rng.uniform(1e-3, 1e-2, N).astype(np.float32)
+    b = rng.uniform(-0.1, 0.1, N).astype(np.float32)
+    out = host(_run(bits, A, W, s_a, s_w, b, mode=mode, gelu=gelu))
+    omode = {M.OUT_F32: oracle.OUT_F32, M.OUT_F16: oracle.OUT_F16, M.OUT_BF16: oracle.OUT_BF16}[mode]
+    ref = oracle.linear(A, W, s_a, s_w, b, mode=omode, gelu=gelu)
+    if mode == M.OUT_F32:
+        assert np.array_equal(out.view(np.uint32), ref.view(np.uint32))
+    else:
+        assert np.array_equal(out.view(np.uint16), ref.view(np.uint16))
+
+
+@pytest.mark.parametrize("bits", [4, 8])
+@pytest.mark.parametrize("Mm,N,K", [(1, 32, 64), (128, 3072, 768), (257, 4096, 1024)])
+def test_gemm_requant_gelu_bitexact(bits, Mm, N, K):
+    rng = np.random.default_rng(5 + Mm)
+    A, W = _codes(rng, Mm, N, K, bits)
+    lo, hi = (-8, 7) if bits == 4 else (-128, 127)
+    s_a = np.float32(0.31)
+    s_w = rng.uniform(1e-3, 5e-3, N).astype(np.float32)
+    b = rng.uniform(-0.1, 0.1, N).astype(np.float32)
+    s_out = np.float32(0.05 if bits == 4 else 0.004)
+    mode = M.OUT_I4 if bits == 4 else M.OUT_I8
+    for gelu in (False, True):
+        out = host(_run(bits, A, W, s_a, s_w, b, mode=mode, gelu=gelu, s_out=s_out, qmin=lo, qmax=hi))
+        ref = oracle.linear(A, W, s_a, s_w, b, mode=oracle.OUT_I4 if bits == 4 else oracle.OUT_I8, gelu=gelu,
+                            s_out=s_out, qmin_out=lo, qmax_out=hi)
+        if bits == 4:
+            assert np.array_equal(out, oracle.pack_int4(ref))
+        else:
+            assert np.array_equal(out.view(np.int8), ref)
+
+
+def test_gemm_worst_case_magnitudes():
+    K = 4096
+    for a, w, exp in [(-8, -7, 229376), (-8, 7, -229376), (7, 7, 200704)]:
+        A = np.full((130, K), a, np.int8)
+        W = np.full((64, K), w, np.int8)
+        out = host(_run(4, A, W, 1.0, np.ones(64, np.float32), None, mode=M.OUT_I32))
+        assert np.all(out == exp)
+    A = np.full((130, K), -128, np.int8)
+    W = np.full((64, K), -127, np.int8)
+    out = host(_run(8, A, W, 1.0, np.ones(64, np.float32), None, mode=M.OUT_I32))
+    assert np.all(out == 66584576)
+
+
+def test_gemm_zero_rows_and_strided():
+    rng = np.random.default_rng(9)
+    A, W = _codes(rng, 100, 256, 512, 4)
+    A[13] = 0
+    Ap = oracle.pack_int4(A)
+    big = np.zeros((100, 512), np.uint8)          # lda = 512 bytes > K/2
+    big[:, :256] = Ap
+    a_t = dev(big)[:, :256]
+    out = torch.zeros((100, 300), dtype=torch.int32, device=DEV)[:, :256]   # ldo > N*4
+    M.mkq_gemm_w4a4(a_t, dev(oracle.pack_int4(W)), 1.0, dev(np.ones(256, np.float32)), None,
+                    mode=M.OUT_I32, out=out, K=512)
+    ref = oracle.gemm_i32(A, W)
+    assert np.array_equal(host(out), ref)
+    assert np.all(host(out)[13] == 0)
+
+
+def test_w8a8_equals_w4a4_when_codes_fit():
+    rng = np.random.default_rng(10)
+    A, W = _codes(rng, 200, 512, 768, 4)
+    o4 = host(_run(4, A, W, 1.0, np.ones(512, np.float32), None, mode=M.OUT_I32))
+    o8 = host(_run(8, A, W, 1.0, np.ones(512, np.float32), None, mode=M.OUT_I32))
+    assert np.array_equal(o4, o8)
+
+
+@pytest.mark.parametrize("N,K", [(4096, 1024), (1024, 4096), (3072, 1024)])
+def test_gemm_full_size_sampled_rows(N, K):
+    """BASELINE configs[3] shapes at full M (131072 rows, the bench launch
+    configuration): GPU computes everything, the oracle a sample of rows."""
+    Mm = 131072
+    rng = np.random.default_rng(N + K)
+    A = rng.integers(-8, 8, (Mm, K)).astype(np.int8)
+    W = rng.integers(-7, 8, (N, K)).astype(np.int8)
+    s_w = rng.uniform(1e-3, 5e-3, N).astype(np.float32)
+    b = rng.uniform(-0.1, 0.1, N).astype(np.float32)
+    Ap = dev(oracle.pack_int4(A))
+    Wp = dev(oracle.pack_int4(W))
+    out = host(M.mkq_gemm_w4a4(Ap, Wp, 0.31, dev(s_w), dev(b), mode=M.OUT_F32, K=K))
+    rows = np.sort(rng.choice(Mm, 48, replace=False))
+    rows[-1] = Mm - 1
+    ref = oracle.linear(A[rows], W, np.float32(0.31), s_w, b, mode=oracle.OUT_F32)
+    assert np.array_equal(out[rows].view(np.uint32), ref.view(np.uint32))
+
+
+# ------------------------------------------------------------------ a8 glue
+def _qkv_fp16(T, hidden, seed):
+    rng = np.random.default_rng(seed)
+    return (rng.standard_normal((T, 3 * hidden)).astype(np.float32) * np.float32(0.8)).astype(np.float16)
+
+
+@pytest.mark.parametrize("seqlens,heads", [([128], 12), ([64, 64], 2), ([1, 17, 130, 5], 4), ([512, 512], 16)])
+def test_attention_vs_oracle(seqlens, heads):
+    T = sum(seqlens)
+    hidden = heads * 64
+    qkv = _qkv_fp16(T, hidden, seed=T)
+    cu = np.concatenate([[0], np.cumsum(seqlens)]).astype(np.int32)
+    uniform = len(set(seqlens)) == 1
+    out = host(M.mkq_attention(dev(qkv), heads, len(seqlens), max(seqlens),
+                               None if uniform else dev(cu), mode=M.OUT_F32))
+    ref = OL.attention(qkv.astype(np.float64), seqlens, heads)
+    err = np.abs(out - ref)
+    assert err.max() < 2e-3 * max(1.0, np.abs(ref).max()), err.max()
+    # fused quantize == oracle quantize of the GPU's own fp32 OA (bit-exact)
+    s = np.float32(0.05)
+    q = host(M.mkq_attention(dev(qkv), heads, len(seqlens), max(seqlens), None if uniform else dev(cu),
+                             mode=M.OUT_I4, s_out=s))
+    assert np.array_equal(q, oracle.pack_int4(oracle.quantize(out, s, -8, 7)))
+
+
+@pytest.mark.parametrize("rows,cols", [(5, 768), (300, 1024), (17, 4096)])
+def test_residual_layernorm(rows, cols):
+    rng = np.random.default_rng(rows + cols)
+    x = rng.standard_normal((rows, cols)).astype(np.float32) * 3
+    r = rng.standard_normal((rows, cols)).astype(np.float32)
+    g, b = synth.ln_params(cols, 3)
+    y, q = M.mkq_residual_layernorm(dev(x), dev(r), dev(g), dev(b), 1e-12, bits=4, s_q=0.5558)
+    y = host(y)
+    ref = OL.layernorm(x.astype(np.float64) + r, g, b)
+    assert np.abs(y - ref).max() < 2e-5 * max(1.0, np.abs(ref).max())
+    assert np.array_equal(host(q), oracle.pack_int4(oracle.quantize(y, np.float32(0.5558), -8, 7)))
+
+
+# ------------------------------------------------------------------ errors on device
+def test_device_errors_surface():
+    with pytest.raises(M.__dict__.get("MkqError", RuntimeError)):
+        M.mkq_gemm_w4a4(torch.zeros((4, 16), dtype=torch.uint8, device=DEV),
+                        torch.zeros((33, 16), dtype=torch.uint8, device=DEV), 1.0,
+                        torch.ones(33, device=DEV))

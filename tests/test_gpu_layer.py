@@ -1,0 +1,122 @@
+"""GPU parity of the full quantized BERT layer (mkq_bert_layer) against the
+fp64 oracle layer: stage-wise replay (each GPU stage fed to the oracle stage;
+codes / int32-derived outputs bit-exact) and end-to-end tolerance."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from oracle import layer as OL
+import synth
+
+pytestmark = pytest.mark.gpu
+
+from paper_2203_13483_b200 import mkq as M  # noqa: E402
+from paper_2203_13483_b200 import model  # noqa: E402
+
+DEV = "cuda:0"
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+def make(hidden, heads, ffn, bits, seqlens, layer=0):
+    p = synth.layer_params(hidden, heads, ffn, layer)
+    W = OL.LayerWeights(hidden, heads, ffn, bits,
+                        OL.prepare_weight(p.w_qkv, p.b_qkv, bits), OL.prepare_weight(p.w_o, p.b_o, bits),
+                        OL.prepare_weight(p.w_1, p.b_1, bits), OL.prepare_weight(p.w_2, p.b_2, bits),
+                        p.ln1_g, p.ln1_b, p.ln2_g, p.ln2_b)
+    hc = synth.activations(sum(seqlens), hidden, seed=1000000 + layer)
+    OL.calibrate(hc, W, seqlens)
+    scales = dict(s_qkv_in=W.s_qkv_in, s_o_in=W.s_o_in, s_ffn1_in=W.s_ffn1_in, s_ffn2_in=W.s_ffn2_in)
+    L = model.build_layer(p, bits, DEV, scales)
+    return p, W, L
+
+
+@pytest.mark.parametrize("bits", [4, 8])
+@pytest.mark.parametrize("seqlens", [[64, 64], [1, 17, 100, 5]])
+def test_layer_stagewise_and_end_to_end(bits, seqlens):
+    hidden, heads, ffn = 256, 4, 1024
+    p, W, L = make(hidden, heads, ffn, bits, seqlens)
+    # product weight prep == oracle weight prep (a0)
+    wq = host(L.t["w_1"])
+    ref_codes = oracle.pack_int4(W.w1.codes) if bits == 4 else W.w1.codes
+    assert np.array_equal(wq.view(ref_codes.dtype), ref_codes)
+    T = sum(seqlens)
+    h = synth.hidden_states(1, T, hidden, seed=5)
+    cu = np.concatenate([[0], np.cumsum(seqlens)]).astype(np.int32)
+    uniform = len(set(seqlens)) == 1
+    cu_d = None if uniform else dev(cu)
+    out = host(M.mkq_bert_layer(L, dev(h), len(seqlens), max(seqlens), cu_d))
+
+    # ---- stage-wise replay through the individual entry points
+    lo, hi = model.act_range(bits)
+    gemm = M.mkq_gemm_w4a4 if bits == 4 else M.mkq_gemm_w8a8
+    pack = (lambda c: oracle.pack_int4(c)) if bits == 4 else (lambda c: c)
+    view = (lambda a: a) if bits == 4 else (lambda a: a.view(np.int8))
+    t = L.t
+    c_in = M.mkq_quantize_pack(dev(h), dev(np.float32([W.s_qkv_in])), bits, lo, hi)
+    assert np.array_equal(view(host(c_in)), pack(oracle.quantize(h, W.s_qkv_in, lo, hi)))
+    qkv = gemm(c_in, t["w_qkv"], W.s_qkv_in, t["sw_qkv"], t["b_qkv"], mode=M.OUT_F16, K=hidden)
+    ref_qkv = oracle.linear(oracle.quantize(h, W.s_qkv_in, lo, hi), W.qkv.codes, W.s_qkv_in, W.qkv.s_w,
+                            W.qkv.bias, mode=oracle.OUT_F16)
+    assert np.array_equal(host(qkv).view(np.uint16), ref_qkv)
+    oa = host(M.mkq_attention(qkv, heads, len(seqlens), max(seqlens), cu_d, mode=M.OUT_F32))
+    ref_oa = OL.attention(ref_qkv.view(np.float16).astype(np.float64), seqlens, heads)
+    assert np.abs(oa - ref_oa).max() < 2e-3 * max(1.0, np.abs(ref_oa).max())
+    c_oa = oracle.quantize(oa, W.s_o_in, lo, hi)
+    o = host(gemm(dev(pack(c_oa)), t["w_o"], W.s_o_in, t["sw_o"], t["b_o"], mode=M.OUT_F32, K=hidden))
+    assert np.array_equal(o, oracle.linear(c_oa, W.o.codes, W.s_o_in, W.o.s_w, W.o.bias))
+    h1, c_h1 = M.mkq_residual_layernorm(dev(o), dev(h), t["ln1_g"], t["ln1_b"], 1e-12, bits=bits,
+                                        s_q=W.s_ffn1_in, qmin=lo, qmax=hi)
+    h1 = host(h1)
+    ref_h1 = OL.layernorm(o.astype(np.float64) + h, W.ln1_g, W.ln1_b)
+    assert np.abs(h1 - ref_h1).max() < 2e-5 * max(1.0, np.abs(ref_h1).max())
+    codes_h1 = oracle.quantize(h1, W.s_ffn1_in, lo, hi)
+    assert np.array_equal(view(host(c_h1)), pack(codes_h1))
+    a2 = gemm(c_h1, t["w_1"], W.s_ffn1_in, t["sw_1"], t["b_1"], mode=M.OUT_I4 if bits == 4 else M.OUT_I8,
+              gelu=True, s_out=W.s_ffn2_in, qmin=lo, qmax=hi, K=hidden)
+    ref_a2 = oracle.linear(codes_h1, W.w1.codes, W.s_ffn1_in, W.w1.s_w, W.w1.bias,
+                           mode=oracle.OUT_I4 if bits == 4 else oracle.OUT_I8, gelu=True, s_out=W.s_ffn2_in,
+                           qmin_out=lo, qmax_out=hi)
+    assert np.array_equal(view(host(a2)), pack(ref_a2))
+    f = host(gemm(a2, t["w_2"], W.s_ffn2_in, t["sw_2"], t["b_2"], mode=M.OUT_F32, K=ffn))
+    assert np.array_equal(f, oracle.linear(ref_a2, W.w2.codes, W.s_ffn2_in, W.w2.s_w, W.w2.bias))
+    y = host(M.mkq_residual_layernorm(dev(f), dev(h1), t["ln2_g"], t["ln2_b"], 1e-12))
+    # the fused layer call runs exactly these kernels: identical bits
+    assert np.array_equal(y, out)
+
+    # ---- end-to-end against the independent fp64 oracle layer
+    T_ = OL.bert_layer(h, W, seqlens)
+    rel = np.sqrt(np.mean((out.astype(np.float64) - T_.h_out) ** 2) / np.mean(T_.h_out.astype(np.float64) ** 2))
+    flips = int(np.sum(oracle.quantize(oa, W.s_o_in, lo, hi) != T_.codes_oa))
+    print(f"bits={bits} seqlens={seqlens} rms_rel={rel:.2e} oa_code_flips={flips}/{T_.codes_oa.size}")
+    assert rel < 5e-3
+    # any code difference is a +-1 flip at a near-tie of the upstream float
+    d = oracle.quantize(oa, W.s_o_in, lo, hi).astype(int) - T_.codes_oa.astype(int)
+    assert np.abs(d).max() <= 1
+
+
+def test_mixed_precision_encoder_runs():
+    """BASELINE configs[2] plan at reduced size: layers 1-2 W8A8, 3-4 W4A4."""
+    plan = model.bit_plan(4, 2)
+    assert plan == [8, 8, 4, 4]
+    assert model.compression_ratio(model.bit_plan(12, 6)) == pytest.approx(32 / 6)
+    seq = [32, 32]
+    layers = []
+    for i, b in enumerate(plan):
+        p = synth.layer_params(128, 2, 512, i)
+        L = model.build_layer(p, b, DEV)
+        model.calibrate(L, dev(synth.activations(64, 128, seed=1000000 + i)), 2, 32)
+        layers.append(L)
+    enc = model.Encoder(layers)
+    h = dev(synth.hidden_states(2, 32, 128, seed=1))
+    out = host(enc(h, 2, 32, out=torch.empty_like(h)))
+    assert np.isfinite(out).all()
+    assert np.allclose(out.mean(-1), 0.0, atol=0.1)
