@@ -23,6 +23,8 @@ def dev(a):
 
 def host(t):
     torch.cuda.synchronize()
+    if t.dtype == torch.bfloat16:
+        t = t.view(torch.int16)
     return t.cpu().numpy()
 
 
