@@ -1,0 +1,452 @@
+#!/usr/bin/env python3
+"""bench.py -- BERT int4 (W4A4) layer throughput on B200, 1..8 GPUs.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    (N > 1: launched by torchrun, one rank per GPU, NCCL for barrier/timing)
+
+Workload (BASELINE.json configs[3], at N=1 exactly that config per rank):
+one BERT-large post-LN encoder layer (hidden 1024, 16 heads, FFN 4096),
+W4A4 on all six weight GEMMs, batch 256 x seq 512 = 131072 tokens per rank,
+synthetic seeded data and random-init weights (synth/).  Scaling is weak:
+every rank runs its own batch of whole sequences (row sharding, no
+data-path collective).
+
+A step is one pass of the whole hot path (§8a rows a1-a8) over one batch:
+mkq_bert_layer = quantize -> QKV GEMM (fp16 out) -> attention (+fused
+quantize) -> W^A GEMM -> residual+LN (+fused quantize) -> FFN1 GEMM (GELU +
+requant fused) -> FFN2 GEMM -> residual+LN.
+
+metric / value: "W4A4 GEMM TOPS" = the layer's linear-GEMM integer ops
+(2*tokens*(3h^2 + h^2 + 2*h*ffn), the BASELINE.md 'effective int4 layer
+throughput' methodology) / layer time, summed over ranks.  Layer latency,
+per-stage times, the dominant kernel's roofline and the paper-style fp32 /
+bf16 layer comparison are reported beside it.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+CFG = dict(batch=256, seq=512, hidden=1024, heads=16, ffn=4096, bits=4)
+WORKLOAD = "bert_large_w4a4_layer_b256_s512 (BASELINE.json configs[3], per rank)"
+
+
+def linear_ops(tokens, hidden, ffn):
+    return 2.0 * tokens * (3 * hidden * hidden + hidden * hidden + 2 * hidden * ffn)
+
+
+def peaks():
+    p = {}
+    try:
+        p = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        src = "measured"
+    except Exception:
+        src = "fallback"
+    hbm = float(p.get("hbm_gbs", 6650.0))
+    bf16_burst = float(p.get("bf16_tflops", 1590.0))
+    bf16_sus = float(p.get("bf16_tflops_sustained", 1400.0))
+    # int8 dense = 2x bf16 dense (nominal 4.5 / 2.25 PFLOP/s; B200_PROFILING.md)
+    return dict(src=src, hbm_gbs=hbm, int8_tops_burst=2 * bf16_burst, int8_tops_sustained=2 * bf16_sus,
+                bf16_tflops=bf16_burst)
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([c.strip() for c in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------ our arm
+def setup_layer(torch, dev, rank):
+    import synth
+    from paper_2203_13483_b200 import model
+    p = synth.layer_params(CFG["hidden"], CFG["heads"], CFG["ffn"], layer=0)
+    L = model.build_layer(p, CFG["bits"], dev)
+    # offline calibration on a 4-sequence calibration batch
+    ncal = 4
+    hc = torch.from_numpy(synth.hidden_states(ncal, CFG["seq"], CFG["hidden"], seed=1000000)).to(dev)
+    model.calibrate(L, hc, ncal, CFG["seq"])
+    return L, p
+
+
+def stage_calls(M, L, h_in, ws, T, stream):
+    """The eight launches of mkq_bert_layer as separate C-ABI calls (same
+    kernels, same arguments) so each can be bracketed by CUDA events."""
+    import torch
+    hd, F, bits = L.hidden, L.ffn, L.bits
+    t = L.t
+    s = L.scales
+    buf = {}
+    dev = h_in.device
+    buf["c_in"] = torch.empty((T, hd // 2), dtype=torch.uint8, device=dev)
+    buf["qkv"] = torch.empty((T, 3 * hd), dtype=torch.float16, device=dev)
+    buf["c_oa"] = torch.empty((T, hd // 2), dtype=torch.uint8, device=dev)
+    buf["o"] = torch.empty((T, hd), dtype=torch.float32, device=dev)
+    buf["h1"] = torch.empty((T, hd), dtype=torch.float32, device=dev)
+    buf["c_h1"] = torch.empty((T, hd // 2), dtype=torch.uint8, device=dev)
+    buf["a2"] = torch.empty((T, F // 2), dtype=torch.uint8, device=dev)
+    buf["f"] = torch.empty((T, hd), dtype=torch.float32, device=dev)
+    buf["out"] = torch.empty((T, hd), dtype=torch.float32, device=dev)
+    sq = torch.tensor([s["s_qkv_in"]], device=dev)
+    B, S = CFG["batch"], CFG["seq"]
+    calls = [
+        ("quantize_in", lambda: M.mkq_quantize_pack(h_in, sq, 4, -8, 7, out=buf["c_in"], stream=stream), 0),
+        ("gemm_qkv", lambda: M.mkq_gemm_w4a4(buf["c_in"], t["w_qkv"], s["s_qkv_in"], t["sw_qkv"], t["b_qkv"],
+                                             mode=M.OUT_F16, out=buf["qkv"], K=hd, stream=stream), 2.0 * T * 3 * hd * hd),
+        ("attention", lambda: M.mkq_attention(buf["qkv"], L.heads, B, S, None, mode=M.OUT_I4, s_out=s["s_o_in"],
+                                              out=buf["c_oa"], stream=stream), 0),
+        ("gemm_o", lambda: M.mkq_gemm_w4a4(buf["c_oa"], t["w_o"], s["s_o_in"], t["sw_o"], t["b_o"], mode=M.OUT_F32,
+                                           out=buf["o"], K=hd, stream=stream), 2.0 * T * hd * hd),
+        ("ln1_quant", lambda: M.mkq_residual_layernorm(buf["o"], h_in, t["ln1_g"], t["ln1_b"], L.ln_eps, bits=4,
+                                                       s_q=s["s_ffn1_in"], y=buf["h1"], q=buf["c_h1"], stream=stream), 0),
+        ("gemm_ffn1", lambda: M.mkq_gemm_w4a4(buf["c_h1"], t["w_1"], s["s_ffn1_in"], t["sw_1"], t["b_1"],
+                                              mode=M.OUT_I4, gelu=True, s_out=s["s_ffn2_in"], out=buf["a2"], K=hd,
+                                              stream=stream), 2.0 * T * hd * F),
+        ("gemm_ffn2", lambda: M.mkq_gemm_w4a4(buf["a2"], t["w_2"], s["s_ffn2_in"], t["sw_2"], t["b_2"],
+                                              mode=M.OUT_F32, out=buf["f"], K=F, stream=stream), 2.0 * T * hd * F),
+        ("ln2", lambda: M.mkq_residual_layernorm(buf["f"], buf["h1"], t["ln2_g"], t["ln2_b"], L.ln_eps,
+                                                 y=buf["out"], stream=stream), 0),
+    ]
+    return calls, buf
+
+
+def stage_bytes(T, hd, F):
+    """Algorithmic HBM bytes per launch."""
+    return {
+        "quantize_in": T * hd * 4.5,
+        "gemm_qkv": T * hd / 2 + 3 * hd * hd / 2 + T * 3 * hd * 2,
+        "attention": T * 3 * hd * 2 + T * hd / 2,
+        "gemm_o": T * hd / 2 + hd * hd / 2 + T * hd * 4,
+        "ln1_quant": T * hd * (4 + 4 + 4 + 0.5),
+        "gemm_ffn1": T * hd / 2 + F * hd / 2 + T * F / 2,
+        "gemm_ffn2": T * F / 2 + F * hd / 2 + T * hd * 4,
+        "ln2": T * hd * 12,
+    }
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2203_13483_b200 import mkq as M
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    import synth
+
+    L, p = setup_layer(torch, dev, rank)
+    B, S, hd, F = CFG["batch"], CFG["seq"], CFG["hidden"], CFG["ffn"]
+    T = B * S
+    h_host = synth.hidden_states(B, S, hd, seed=rank)
+    h_in = torch.from_numpy(h_host).to(dev)
+    h_out = torch.empty_like(h_in)
+    ws = torch.empty(L.workspace_size(T), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.Stream(device=dev)
+
+    def step():
+        M.mkq_bert_layer(L, h_in, B, S, None, h_out=h_out, ws=ws, stream=stream)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step()
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        time.sleep(0.3)
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        barrier()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    t_max = ms
+    if world > 1:
+        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_max = float(tt.item())
+    ops = linear_ops(T, hd, F)
+    value = world * ops / (t_max * 1e-3) / 1e12
+
+    # ---- per-stage device times (same kernels, one event pair per launch)
+    calls, buf = stage_calls(M, L, h_in, ws, T, stream)
+    nrep = max(3, min(args.steps, 10))
+    evs = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in calls]
+           for _ in range(nrep)]
+    with torch.cuda.stream(stream):
+        for c in calls:
+            c[1]()
+        torch.cuda.synchronize(dev)
+        for r in range(nrep):
+            for i, c in enumerate(calls):
+                evs[r][i][0].record(stream)
+                c[1]()
+                evs[r][i][1].record(stream)
+    torch.cuda.synchronize(dev)
+    stage_ms = {c[0]: float(np.mean([evs[r][i][0].elapsed_time(evs[r][i][1]) for r in range(nrep)]))
+                for i, c in enumerate(calls)}
+    same = bool(torch.equal(buf["out"], h_out))
+    pk = peaks()
+    sb = stage_bytes(T, hd, F)
+    gemms = {k: v for k, v in stage_ms.items() if k.startswith("gemm")}
+    dom = max(stage_ms, key=stage_ms.get)
+    ops_of = {c[0]: c[2] for c in calls}
+    if ops_of[dom] > 0:
+        ach = ops_of[dom] / (stage_ms[dom] * 1e-3) / 1e12
+        roof = {"kernel": dom, "bound": "tensor", "achieved": round(ach, 1),
+                "peak": round(pk["int8_tops_sustained"], 1), "unit": "TOPS (int8 dense)",
+                "frac": round(ach / pk["int8_tops_sustained"], 4), "traffic": None,
+                "peak_src": f"{pk['src']} bf16_tflops_sustained x2 (int8:bf16 nominal 4.5:2.25)"}
+    else:
+        ach = sb[dom] / (stage_ms[dom] * 1e-3) / 1e9
+        roof = {"kernel": dom, "bound": "hbm", "achieved": round(ach, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": round(ach / pk["hbm_gbs"], 4), "traffic": None, "peak_src": pk["src"] + " hbm_gbs"}
+    stages = {}
+    for k, v in stage_ms.items():
+        d = {"us": round(v * 1e3, 1), "share": round(v / sum(stage_ms.values()), 3),
+             "gbs": round(sb[k] / (v * 1e-3) / 1e9, 1)}
+        if ops_of[k]:
+            d["tops"] = round(ops_of[k] / (v * 1e-3) / 1e12, 1)
+            d["frac_int8_peak"] = round(ops_of[k] / (v * 1e-3) / 1e12 / pk["int8_tops_sustained"], 3)
+        stages[k] = d
+    gemm_ms = sum(gemms.values())
+    gemm_tops = ops / (gemm_ms * 1e-3) / 1e12
+
+    # ---- e2e: host buffers through the C-ABI, H2D + layer + D2H in the timed region
+    h_pin = torch.from_numpy(h_host).pin_memory()
+    o_pin = torch.empty(h_host.shape, dtype=torch.float32).pin_memory()
+    e2e_steps = max(2, min(args.steps, 5))
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for _ in range(e2e_steps):
+            h_in.copy_(h_pin, non_blocking=True)
+            M.mkq_bert_layer(L, h_in, B, S, None, h_out=h_out, ws=ws, stream=stream)
+            o_pin.copy_(h_out, non_blocking=True)
+        e1.record(stream)
+    barrier()
+    e2e_ms = e0.elapsed_time(e1) / e2e_steps
+    if world > 1:
+        tt = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+
+    # ---- paper-style comparison arm: fp32 / bf16 torch layer
+    cmp = None
+    if rank == 0 and not args.no_compare:
+        cmp = compare_float_layers(torch, p, dev, ms, args)
+
+    result = None
+    if rank == 0:
+        cpu = None if (args.no_cpu or world > 1) else cpu_baseline(sample_seqs=1)
+        result = {
+            "metric": "W4A4 GEMM TOPS (effective: layer linear-GEMM int ops / BERT int4 layer time)",
+            "value": round(value, 2),
+            "unit": "TOPS",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": round(t_max, 4),
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "s4 x s4 -> s32 (int8 tcgen05), fp32 epilogue/LN, fp16 attention",
+            "data": "synthetic (seeded N(0,1) activations, N(0,0.02^2) random-init BERT weights)",
+            "config": {"workload": WORKLOAD, "batch_per_rank": B, "seq_len": S, "hidden": hd, "heads": CFG["heads"],
+                       "ffn": F, "bits": 4, "tokens_per_rank": T, "parallelism": f"row-shard x{world} (no collective)",
+                       "l2": "inputs > L2: 537 MB fp32 activations + ~3 GB intermediates per step; weights (6.3 MB) L2-resident"},
+            "layer_latency_us": round(t_max * 1e3, 1),
+            "gemm_only_tops": round(gemm_tops, 1),
+            "stages": stages,
+            "layer_equals_staged": same,
+            "roofline": roof,
+            "e2e": {"value": round(world * ops / (e2e_ms * 1e-3) / 1e12, 2), "unit": "TOPS",
+                    "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": int(h_host.nbytes),
+                    "d2h_bytes_per_step": int(h_host.nbytes)},
+            "gpu_launches": 8 * args.steps,
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+            "paper_comparison": cmp,
+        }
+        print(json.dumps(result))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return result
+
+
+def compare_float_layers(torch, p, dev, int4_ms, args):
+    """fp32 (TF32 off) and bf16 torch/cuBLAS BERT-large layer on the same
+    shape, for the paper's int4-vs-fp32 speedup methodology (Table 2)."""
+    import torch.nn.functional as Fn
+    B, S, hd, H, F = CFG["batch"], CFG["seq"], CFG["hidden"], CFG["heads"], CFG["ffn"]
+    torch.backends.cuda.matmul.allow_tf32 = False
+    torch.backends.cudnn.allow_tf32 = False
+    out = {}
+    for dt in (torch.float32, torch.bfloat16):
+        W = {k: torch.from_numpy(getattr(p, k)).to(dev, dt) for k in
+             ("w_qkv", "b_qkv", "w_o", "b_o", "w_1", "b_1", "w_2", "b_2", "ln1_g", "ln1_b", "ln2_g", "ln2_b")}
+        chunk = 32
+        x = torch.randn(chunk * S, hd, device=dev, dtype=dt)
+
+        def layer(h):
+            qkv = Fn.linear(h, W["w_qkv"], W["b_qkv"]).view(chunk, S, 3, H, 64)
+            q, k, v = qkv.unbind(2)
+            a = Fn.scaled_dot_product_attention(q.transpose(1, 2), k.transpose(1, 2), v.transpose(1, 2))
+            a = a.transpose(1, 2).reshape(chunk * S, hd)
+            h1 = Fn.layer_norm(Fn.linear(a, W["w_o"], W["b_o"]) + h, (hd,), W["ln1_g"], W["ln1_b"], 1e-12)
+            f = Fn.linear(Fn.gelu(Fn.linear(h1, W["w_1"], W["b_1"])), W["w_2"], W["b_2"])
+            return Fn.layer_norm(f + h1, (hd,), W["ln2_g"], W["ln2_b"], 1e-12)
+
+        for _ in range(2):
+            layer(x)
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 2
+        e0.record()
+        for _ in range(reps):
+            for _c in range(B // chunk):
+                layer(x)
+        e1.record()
+        torch.cuda.synchronize(dev)
+        out["fp32_layer_ms" if dt == torch.float32 else "bf16_layer_ms"] = round(e0.elapsed_time(e1) / reps, 3)
+        del W, x
+    out["int4_layer_ms"] = round(int4_ms, 3)
+    out["speedup_int4_vs_fp32"] = round(out["fp32_layer_ms"] / int4_ms, 2)
+    out["speedup_int4_vs_bf16"] = round(out["bf16_layer_ms"] / int4_ms, 2)
+    out["paper_context"] = "MKQ-BERT Table 2 (P:250-264): int4 15x vs fp32 for one BERT-base layer, NVIDIA T4, BS64"
+    torch.backends.cuda.matmul.allow_tf32 = True
+    return out
+
+
+# ------------------------------------------------------------------ oracle (CPU) arm
+def cpu_baseline(sample_seqs=1):
+    """The oracle as it stands, on the host cores, over a bounded sample of
+    the same workload (whole sequences of the BERT-large layer)."""
+    import oracle
+    from oracle import layer as OL
+    import synth
+    hd, H, F, S = CFG["hidden"], CFG["heads"], CFG["ffn"], CFG["seq"]
+    p = synth.layer_params(hd, H, F, 0)
+    W = OL.LayerWeights(hd, H, F, 4, OL.prepare_weight(p.w_qkv, p.b_qkv, 4), OL.prepare_weight(p.w_o, p.b_o, 4),
+                        OL.prepare_weight(p.w_1, p.b_1, 4), OL.prepare_weight(p.w_2, p.b_2, 4),
+                        p.ln1_g, p.ln1_b, p.ln2_g, p.ln2_b)
+    W.s_qkv_in = W.s_o_in = W.s_ffn1_in = np.float32(3.8906 / 7)
+    W.s_ffn2_in = np.float32(0.5)
+    h = synth.hidden_states(sample_seqs, S, hd, seed=0)
+    oracle.build()
+    t0 = time.perf_counter()
+    OL.bert_layer(h, W, [S] * sample_seqs)
+    dt = time.perf_counter() - t0
+    T = sample_seqs * S
+    return {"value": round(linear_ops(T, hd, F) / dt / 1e12, 6), "unit": "TOPS", "cores": 1, "kind": "oracle",
+            "sample": f"{sample_seqs} x {S}-token sequence(s) of the BERT-large W4A4 layer (oracle/: scalar C int "
+                      f"GEMM + fp64 NumPy glue, single thread), {dt:.2f} s",
+            "seconds": round(dt, 3)}
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    vals = []
+    for _ in range(args.warmup if args.warmup < 1 else 1):
+        cpu_baseline(1)
+    for _ in range(args.steps):
+        vals.append(cpu_baseline(1))
+    v = float(np.mean([c["value"] for c in vals]))
+    sec = float(np.mean([c["seconds"] for c in vals]))
+    res = {
+        "impl": "reference",
+        "metric": "W4A4 GEMM TOPS (effective: layer linear-GEMM int ops / BERT int4 layer time)",
+        "value": round(v, 6), "unit": "TOPS", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(sec * 1e3, 1), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "s4 x s4 -> s32 (scalar C), fp64 glue", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "sample": "1 sequence of 512 tokens per step"},
+        "cpu_baseline": {"value": round(v, 6), "unit": "TOPS", "cores": 1, "kind": "oracle",
+                         "sample": "1 x 512-token sequence per step"},
+        "e2e": {"value": round(v, 6), "unit": "TOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(res))
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-compare", action="store_true", help="skip the fp32/bf16 torch comparison layer")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the oracle cpu_baseline")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

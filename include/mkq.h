@@ -88,7 +88,25 @@ typedef struct {
     float s_out;       /* requantization scale (I4/I8 only), > 0, finite   */
     int32_t qmin_out;  /* requantization code range (I4/I8 only)           */
     int32_t qmax_out;
+    /* Optional [device] table from mkq_requant_table() built for exactly
+     * (gelu, s_out, qmin_out, qmax_out); NULL = evaluate gelu_pinned and the
+     * division per output.  Results are bit-identical either way (the table
+     * is exact by construction and self-verified; an invalid table is
+     * ignored on the device). */
+    const void *requant_table;
 } mkq_epilogue;
+
+/* Bytes of a requant table (device buffer, caller-owned, 16-byte aligned). */
+MKQ_API size_t mkq_requant_table_size(void);
+
+/* Build the exact y-space lookup table of the fused requantize epilogue
+ * (§8a-a5/a6; DESIGN.md §5 "requant table"):  for every fp32 y,
+ *     code(y) = clamp(rint_even((gelu ? gelu_pinned(y) : y) / s_out), qmin, qmax)
+ * is tabulated as per-cell thresholds, found by evaluating code(y) for every
+ * float where it can change.  Asynchronous on `stream`; needs
+ * qmin <= 0 <= qmax.  The table depends only on (gelu, s_out, qmin, qmax). */
+MKQ_API mkq_status mkq_requant_table(int gelu, float s_out, int qmin, int qmax, void *table,
+                                     size_t table_bytes, void *stream);
 
 /* ------------------------------------------------------------------------
  * §8a-a1: activation (or weight) quantize + pack, Eq.1:
@@ -196,6 +214,9 @@ typedef struct {
     const float *ln1_g, *ln1_b, *ln2_g, *ln2_b;
     float s_qkv_in, s_o_in, s_ffn1_in, s_ffn2_in;
     float ln_eps;
+    /* optional [device] mkq_requant_table(1, s_ffn2_in, qmin, qmax) for the
+     * FFN1 epilogue (NULL = direct evaluation; identical results) */
+    const void *ffn1_requant_table;
 } mkq_layer;
 
 /* Workspace bytes for `tokens` rows (intermediates of one layer). */

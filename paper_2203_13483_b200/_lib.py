@@ -6,7 +6,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SO = os.path.join(HERE, "libmkq.so")
+SO = os.environ.get("MKQ_LIB") or os.path.join(HERE, "libmkq.so")
 
 P = ctypes.c_void_p
 I64 = ctypes.c_int64
@@ -30,6 +30,8 @@ SIGNATURES = {
     "mkq_gemm_w4a4": (I32, [P, I64, P, I64, I64, I64, I64, F32, P, P, P, P, I64, P, SZ, P]),
     "mkq_gemm_w8a8": (I32, [P, I64, P, I64, I64, I64, I64, F32, P, P, P, P, I64, P, SZ, P]),
     "mkq_gemm_workspace_size": (SZ, [I64, I64, I64]),
+    "mkq_requant_table_size": (SZ, []),
+    "mkq_requant_table": (I32, [I32, F32, I32, I32, P, SZ, P]),
     "mkq_attention": (I32, [P, I64, I64, I64, P, I64, I32, I32, I32, F32, I32, I32, P, I64, P]),
     "mkq_residual_layernorm": (I32, [P, P, I64, I64, I64, P, P, F32, P, I32, F32, I32, I32, P, I64, P]),
     "mkq_bert_layer_workspace_size": (SZ, [P, I64]),
@@ -39,7 +41,7 @@ SIGNATURES = {
 
 class MkqEpilogue(ctypes.Structure):
     _fields_ = [("out", ctypes.c_int32), ("gelu", ctypes.c_int32), ("s_out", ctypes.c_float),
-                ("qmin_out", ctypes.c_int32), ("qmax_out", ctypes.c_int32)]
+                ("qmin_out", ctypes.c_int32), ("qmax_out", ctypes.c_int32), ("requant_table", ctypes.c_void_p)]
 
 
 class MkqLayer(ctypes.Structure):
@@ -47,7 +49,8 @@ class MkqLayer(ctypes.Structure):
                 ("bits", ctypes.c_int32)] + \
         [(n, ctypes.c_void_p) for n in ("w_qkv", "w_o", "w_1", "w_2", "sw_qkv", "sw_o", "sw_1", "sw_2",
                                         "b_qkv", "b_o", "b_1", "b_2", "ln1_g", "ln1_b", "ln2_g", "ln2_b")] + \
-        [(n, ctypes.c_float) for n in ("s_qkv_in", "s_o_in", "s_ffn1_in", "s_ffn2_in", "ln_eps")]
+        [(n, ctypes.c_float) for n in ("s_qkv_in", "s_o_in", "s_ffn1_in", "s_ffn2_in", "ln_eps")] + \
+        [("ffn1_requant_table", ctypes.c_void_p)]
 
 
 class MkqError(RuntimeError):

@@ -1,0 +1,443 @@
+// gemm2_sm100.cuh -- W4A4 GEMM on a CTA pair (cta_group::2): the large-M
+// path of mkq_gemm_w4a4 (§8a rows a2-a6).
+//
+// Same arithmetic as gemm_sm100.cuh (exact int32 accumulation of 16a x 16w,
+// acc >> 8, pinned epilogue), re-tiled for the B200 tensor core:
+//   * a cluster of 2 CTAs on one TPC computes a 256 x BN output tile with
+//     tcgen05.mma.cta_group::2 (M = 256): each CTA stages 128 rows of A and
+//     BN/2 rows of W, so the shared-memory traffic per MMA (TMA write +
+//     unpack LDS/STS + tensor-core read) per SM is 2/3 of the 1-CTA
+//     128 x 256 tile;
+//   * 8 unpack warps per CTA (4 x 16-byte chunks per thread per stage, all
+//     loads issued before any store);
+//   * 8 epilogue warps per CTA (2 per TMEM lane quadrant, each half the
+//     columns), per-tile scale/bias staged in shared memory, TMEM read in
+//     16-column slices, and the exact y-space requant table (requant.cuh)
+//     for the fused GELU + requantize output;
+//   * double-buffered TMEM accumulators (2 x BN columns per CTA) so the
+//     epilogue of tile i overlaps the mainloop of tile i+1.
+// Barriers that gate the MMA (int8 stage full, accumulator empty) live in the
+// leader CTA (rank 0) and collect arrivals from both CTAs; MMA completion is
+// multicast to both CTAs' barriers.
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include "epilogue.cuh"
+#include "gemm_sm100.cuh"
+#include "ptx.cuh"
+#include "requant.cuh"
+
+namespace mkq {
+
+struct Epi2Params {
+    EpiParams e;
+    const void* table;   // rq table (global) or null
+};
+
+template <int BN_>
+struct Gemm2Cfg {
+    static constexpr int BM = 128;                  // A rows per CTA (MMA M = 256 per pair)
+    static constexpr int BN = BN_;                  // MMA N (per pair)
+    static constexpr int BNH = BN / 2;              // W rows per CTA
+    static constexpr int BK = 128;
+    static constexpr int kA8 = BM * BK;
+    static constexpr int kB8 = BNH * BK;
+    static constexpr int kStage8 = kA8 + kB8;
+    static constexpr int kAP = BM * BK / 2;
+    static constexpr int kBP = BNH * BK / 2;
+    static constexpr int kStageP = kAP + kBP;
+    static constexpr int S8 = 4;
+    static constexpr int SP = 3;
+    static constexpr int kEpiWarps = 8;
+    static constexpr int kUnpWarps = 8;
+    static constexpr int kThreads = 32 * (4 + kEpiWarps + kUnpWarps);
+    static constexpr uint32_t kTmemCols = 2 * BN;
+    static constexpr int kScb = 2 * BN * 8;          // 2 buffers x BN x (sc, b)
+    static constexpr int kStaging = kEpiWarps * 4096; // 32 rows x 128 B output block per warp
+    static constexpr int kBarBytes = 8 * (3 * S8 + 2 * SP + 6) + 16;
+    static constexpr int kSmem = 1024 + S8 * kStage8 + SP * kStageP + (int)rq::kSmemBytes + kScb + kStaging + kBarBytes;
+    static_assert(kSmem <= 232448, "shared memory budget");
+    static_assert(BN == 256 || BN == 128, "BN");
+    static_assert((S8 * kStage8 + SP * kStageP) % 1024 == 0, "staging must be 1024-aligned (SWIZZLE_128B)");
+};
+
+// Requant table: header fields in registers, cells in shared memory (read
+// with explicit ld.shared).  Cells clamp at both ends, so y < y_lo and
+// y >= y_hi need no special case: cell 0's "below" code is code_lo and the
+// last cell's "above" code is code_hi.
+struct Lut {
+    float y_lo, inv_w;
+    int ncell;
+    uint32_t cells;   // shared-window address of cell 0
+};
+
+__device__ __noinline__ int requant_direct(float y, int gelu, float s, int qmin, int qmax) {
+    return rq::direct_code(y, gelu, s, qmin, qmax);
+}
+
+__device__ __forceinline__ uint2 lds64(uint32_t addr) {
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ float4 lds128f(uint32_t addr) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+    return v;
+}
+
+// 16 requantized codes (low byte of each q[i] is the two's-complement code).
+__device__ __forceinline__ void lut_codes16(const Lut& L, const EpiParams& ep, const float (&y)[16], uint32_t (&q)[16]) {
+    uint32_t dmask = 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        const uint2 e = lds64(L.cells + 8u * (uint32_t)rq::cell_of(y[i], L.y_lo, L.inv_w, L.ncell));
+        q[i] = y[i] >= __uint_as_float(e.x) ? (e.y >> 8) : e.y;
+        dmask |= (e.y >> 16 & 1u) << i;
+    }
+    if (__builtin_expect(__any_sync(0xffffffffu, dmask != 0), 0)) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+            if (dmask >> i & 1u) q[i] = (uint32_t)requant_direct(y[i], ep.gelu, ep.s_out, ep.qmin, ep.qmax);
+    }
+}
+
+// Byte offset of 16-byte chunk c of staging row r for a row pitch P bytes
+// (the TMA SWIZZLE_{128,64,32}B pattern for P = 128/64/32; none for 16).
+__device__ __forceinline__ uint32_t stg_off(int r, int c, int P) {
+    const int f = P == 128 ? (r & 7) : (P == 64 ? ((r >> 1) & 3) : (P == 32 ? ((r >> 2) & 1) : 0));
+    return (uint32_t)(r * P + ((c ^ f) << 4));
+}
+
+__device__ __forceinline__ int out_pitch(int mode) {   // bytes per row of a 32-column block
+    return mode == OUT_F32 || mode == OUT_I32 ? 128 : (mode == OUT_I4 ? 16 : (mode == OUT_I8 ? 32 : 64));
+}
+
+// 16 outputs (columns cl..cl+15 of one accumulator row) -> staging row `r`,
+// half `h2` of the 32-column block.
+__device__ __forceinline__ void epi2_half(const EpiParams& ep, const Lut& L, bool use_table, uint32_t scb,
+                                          const uint32_t (&v)[16], uint8_t* stage, int r, int h2) {
+    int32_t acc[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc[i] = (int32_t)v[i] >> 8;
+    const int mode = ep.mode;
+    const int P = out_pitch(mode);
+    if (mode == OUT_I32) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+            *reinterpret_cast<int4*>(stage + stg_off(r, h2 * 4 + c, P)) =
+                make_int4(acc[4 * c], acc[4 * c + 1], acc[4 * c + 2], acc[4 * c + 3]);
+        return;
+    }
+    const bool hb = ep.bias != nullptr;
+    float y[16];
+#pragma unroll
+    for (int i = 0; i < 16; i += 2) {
+        const float4 sb = lds128f(scb + 8u * (uint32_t)i);   // (sc, b) of two columns, broadcast
+        y[i] = dequant(acc[i], sb.x, sb.y, hb);
+        y[i + 1] = dequant(acc[i + 1], sb.z, sb.w, hb);
+    }
+    if (mode == OUT_I4 || mode == OUT_I8) {
+        uint32_t q[16];
+        if (use_table) {
+            lut_codes16(L, ep, y, q);
+        } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+                q[i] = (uint32_t)quant_code(ep.gelu ? gelu_pinned(y[i]) : y[i], ep.s_out, ep.qmin, ep.qmax);
+        }
+        if (mode == OUT_I4) {
+            uint32_t a = 0, b = 0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                a |= (q[i] & 0xFu) << (4 * i);
+                b |= (q[8 + i] & 0xFu) << (4 * i);
+            }
+            *reinterpret_cast<uint2*>(stage + r * 16 + h2 * 8) = make_uint2(a, b);
+        } else {
+            uint32_t w[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                w[i] = __byte_perm(__byte_perm(q[4 * i], q[4 * i + 1], 0x0040), __byte_perm(q[4 * i + 2], q[4 * i + 3], 0x0040),
+                                   0x5410);
+            *reinterpret_cast<uint4*>(stage + stg_off(r, h2, P)) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+        return;
+    }
+    if (ep.gelu) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) y[i] = gelu_pinned(y[i]);
+    }
+    if (mode == OUT_F32) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+            *reinterpret_cast<float4*>(stage + stg_off(r, h2 * 4 + c, P)) =
+                make_float4(y[4 * c], y[4 * c + 1], y[4 * c + 2], y[4 * c + 3]);
+    } else {
+        uint32_t w[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            w[i] = mode == OUT_BF16 ? pack_bf16x2(y[2 * i], y[2 * i + 1]) : pack_f16x2(y[2 * i], y[2 * i + 1]);
+        *reinterpret_cast<uint4*>(stage + stg_off(r, h2 * 2, P)) = make_uint4(w[0], w[1], w[2], w[3]);
+        *reinterpret_cast<uint4*>(stage + stg_off(r, h2 * 2 + 1, P)) = make_uint4(w[4], w[5], w[6], w[7]);
+    }
+}
+
+template <class Cfg>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
+    gemm_w4a4_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                          const __grid_constant__ CUtensorMap tmO, const Epi2Params p, int M, int N, int K) {
+    constexpr int BM = Cfg::BM, BN = Cfg::BN, BNH = Cfg::BNH, S8 = Cfg::S8, SP = Cfg::SP;
+    constexpr int kEpiThreads = 32 * Cfg::kEpiWarps;
+    constexpr int kUnpThreads = 32 * Cfg::kUnpWarps;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* ring8 = smem;
+    uint8_t* ringP = ring8 + S8 * Cfg::kStage8;
+    uint8_t* staging = ringP + SP * Cfg::kStageP;   // 1024-aligned, 4 KB per epilogue warp
+    rq::Header* th = reinterpret_cast<rq::Header*>(staging + Cfg::kStaging);
+    uint2* tcells = reinterpret_cast<uint2*>(th + 1);
+    float2* scb = reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(th) + rq::kSmemBytes);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(scb) + Cfg::kScb);
+    uint64_t* full8 = bars;
+    uint64_t* empty8 = full8 + S8;
+    uint64_t* fullP = empty8 + S8;
+    uint64_t* emptyP = fullP + SP;
+    uint64_t* tfull = emptyP + SP;
+    uint64_t* tempty = tfull + 2;
+    uint64_t* ready8 = tempty + 2;   // local: unpack warps -> relay
+    uint64_t* tdone = ready8 + S8;   // local: epilogue warps -> relay
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tdone + 2);
+
+    const EpiParams& ep = p.e;
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t rank = ptx::cluster_ctarank();
+    const int cluster = blockIdx.x >> 1;
+    const int nclusters = gridDim.x >> 1;
+    const int m_tiles = (M + 2 * BM - 1) / (2 * BM);
+    const int n_tiles = (N + BN - 1) / BN;
+    const int num_tiles = m_tiles * n_tiles;
+    const int nk = (K + Cfg::BK - 1) / Cfg::BK;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < S8; ++i) {
+            ptx::mbar_init(&full8[i], 2);                 // one relay arrive per CTA
+            ptx::mbar_init(&empty8[i], 1);
+            ptx::mbar_init(&ready8[i], Cfg::kUnpWarps);
+        }
+        for (int i = 0; i < SP; ++i) {
+            ptx::mbar_init(&fullP[i], 1);
+            ptx::mbar_init(&emptyP[i], kUnpThreads);
+        }
+        for (int i = 0; i < 2; ++i) {
+            ptx::mbar_init(&tfull[i], 1);
+            ptx::mbar_init(&tempty[i], 2);
+            ptx::mbar_init(&tdone[i], Cfg::kEpiWarps);
+        }
+        ptx::fence_barrier_init();
+    }
+    if (warp == 0 && lane == 0) {
+        ptx::tma_prefetch_desc(&tmA);
+        ptx::tma_prefetch_desc(&tmB);
+    }
+    if (warp == 2) ptx::tmem_alloc_2cta<Cfg::kTmemCols>(tmem_slot);
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ---------------------------------------------------- TMA producer (both CTAs)
+        if (lane == 0) {
+            int s = 0;
+            uint32_t ph = 0;
+            for (int tile = cluster; tile < num_tiles; tile += nclusters) {
+                const int m0 = (tile / n_tiles) * 2 * BM + (int)rank * BM;
+                const int n0 = (tile % n_tiles) * BN + (int)rank * BNH;
+                for (int kb = 0; kb < nk; ++kb) {
+                    ptx::mbar_wait(&emptyP[s], ph ^ 1);
+                    uint8_t* dst = ringP + s * Cfg::kStageP;
+                    ptx::mbar_arrive_expect_tx(&fullP[s], Cfg::kStageP);
+                    ptx::tma_load_2d(&tmA, &fullP[s], dst, kb * (Cfg::BK / 2), m0);
+                    ptx::tma_load_2d(&tmB, &fullP[s], dst + Cfg::kAP, kb * (Cfg::BK / 2), n0);
+                    if (++s == SP) { s = 0; ph ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------------------------------------------- MMA issuer (leader CTA)
+        if (rank == 0 && lane == 0) {
+            constexpr uint32_t idesc = ptx::idesc_i8(2 * BM, BN);
+            int s = 0;
+            uint32_t ph = 0;
+            int it = 0;
+            for (int tile = cluster; tile < num_tiles; tile += nclusters, ++it) {
+                const int ab = it & 1;
+                const uint32_t aph = (it >> 1) & 1;
+                ptx::mbar_wait(&tempty[ab], aph ^ 1);
+                ptx::tc_fence_after();
+                const uint32_t d = tmem_base + ab * BN;
+                for (int kb = 0; kb < nk; ++kb) {
+                    ptx::mbar_wait(&full8[s], ph);
+                    ptx::tc_fence_after();
+                    const uint32_t a_addr = ptx::smem_u32(ring8 + s * Cfg::kStage8);
+                    const uint32_t b_addr = a_addr + Cfg::kA8;
+#pragma unroll
+                    for (int k = 0; k < Cfg::BK / 32; ++k)
+                        ptx::mma_i8_ss_2cta(d, ptx::desc_sw128_kmajor(a_addr + 32 * k),
+                                            ptx::desc_sw128_kmajor(b_addr + 32 * k), idesc, (kb | k) != 0);
+                    ptx::mma_commit_2cta_mc(&empty8[s], 3);
+                    if (++s == S8) { s = 0; ph ^= 1; }
+                }
+                ptx::mma_commit_2cta_mc(&tfull[ab], 3);
+            }
+        }
+    } else if (warp == 3) {
+        // ---------------------------------------------------- relay: unpack -> leader
+        // Local (CTA-scope) arrivals of the 8 unpack warps are forwarded to the
+        // leader's full barrier with ONE cluster-scope release per stage (a
+        // cluster-scope release is a GPU-scope membar in SASS).
+        if (lane == 0) {
+            int s8 = 0;
+            uint32_t ph8 = 0;
+            for (int tile = cluster; tile < num_tiles; tile += nclusters)
+                for (int kb = 0; kb < nk; ++kb) {
+                    ptx::mbar_wait(&ready8[s8], ph8);
+                    ptx::mbar_arrive_cluster(ptx::mapa(&full8[s8], 0));
+                    if (++s8 == S8) { s8 = 0; ph8 ^= 1; }
+                }
+        }
+    } else if (warp == 2) {
+        // ---------------------------------------------------- relay: epilogue -> leader
+        if (lane == 0) {
+            int it = 0;
+            for (int tile = cluster; tile < num_tiles; tile += nclusters, ++it) {
+                const int ab = it & 1;
+                ptx::mbar_wait(&tdone[ab], (it >> 1) & 1);
+                ptx::tc_fence_after();
+                ptx::tc_fence_before();
+                ptx::mbar_arrive_cluster(ptx::mapa(&tempty[ab], 0));
+            }
+        }
+    } else if (warp >= 4 && warp < 4 + Cfg::kEpiWarps) {
+        // ---------------------------------------------------- epilogue (both CTAs)
+        const int e = warp - 4;           // 0..7
+        const int q = warp & 3;           // TMEM lane quadrant (warp % 4)
+        const int h = e >> 2;             // column half
+        const int et = threadIdx.x - 128; // 0..255
+        bool use_table = false;
+        if (p.table) {
+            const uint32_t* src = reinterpret_cast<const uint32_t*>(p.table);
+            uint32_t* dst = reinterpret_cast<uint32_t*>(th);
+            for (int i = et; i < (int)(rq::kSmemBytes / 4); i += kEpiThreads) dst[i] = src[i];
+        }
+        ptx::named_bar_sync(1, kEpiThreads);
+        if (p.table)
+            use_table = th->valid != 0 && th->gelu == ep.gelu && th->s_out == ep.s_out && th->qmin == ep.qmin &&
+                        th->qmax == ep.qmax;
+        Lut L{0.0f, 0.0f, 1, ptx::smem_u32(tcells)};
+        if (use_table) L = Lut{th->y_lo, th->inv_w, th->ncell, ptx::smem_u32(tcells)};
+        uint8_t* stage = staging + e * 4096;
+        if (lane == 0) ptx::tma_prefetch_desc(&tmO);
+        int it = 0;
+        for (int tile = cluster; tile < num_tiles; tile += nclusters, ++it) {
+            const int m0 = (tile / n_tiles) * 2 * BM + (int)rank * BM;
+            const int n0 = (tile % n_tiles) * BN;
+            const int ab = it & 1;
+            const uint32_t aph = (it >> 1) & 1;
+            float2* sb = scb + ab * BN;
+            {   // per-column scale and bias of this tile
+                const int n = n0 + et;
+                if (et < BN && n < N)
+                    sb[et] = make_float2(__fmul_rn(ep.s_a, __ldg(ep.s_w + n)), ep.bias ? __ldg(ep.bias + n) : 0.0f);
+            }
+            ptx::named_bar_sync(1, kEpiThreads);
+            ptx::mbar_wait(&tfull[ab], aph);
+            ptx::tc_fence_after();
+            const int row0 = m0 + q * 32;
+#pragma unroll 1
+            for (int j = 0; j < BN / 2 / 32; ++j) {
+                const int cl = h * (BN / 2) + 32 * j;
+                const int n = n0 + cl;
+                if (n >= N) break;
+                // the previous TMA store must have finished reading the staging block
+                if (lane == 0) ptx::tma_store_wait_read<0>();
+                __syncwarp();
+#pragma unroll
+                for (int h2 = 0; h2 < 2; ++h2) {
+                    uint32_t v[16];
+                    ptx::tmem_ld_32x32b_x16(tmem_base + ((uint32_t)(q * 32) << 16) + ab * BN + cl + 16 * h2, v);
+                    ptx::tmem_ld_wait();
+                    epi2_half(ep, L, use_table, ptx::smem_u32(sb + cl + 16 * h2), v, stage, lane, h2);
+                }
+                ptx::fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    ptx::tma_store_2d(&tmO, stage, ep.mode == OUT_I4 ? n / 2 : n, row0);
+                    ptx::tma_store_commit();
+                }
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&tdone[ab]);
+        }
+        if (lane == 0) ptx::tma_store_wait<0>();
+    } else if (warp >= 4 + Cfg::kEpiWarps) {
+        // ---------------------------------------------------- int4 -> int8 unpack (both CTAs)
+        const int u = threadIdx.x - 32 * (4 + Cfg::kEpiWarps);
+        constexpr int kChunks = (BM + BNH) * (Cfg::BK / 32);   // 16-byte packed chunks per stage
+        constexpr int kPer = kChunks / kUnpThreads;
+        static_assert(kChunks % kUnpThreads == 0, "chunk split");
+        int sp = 0, s8 = 0;
+        uint32_t php = 0, ph8 = 0;
+        for (int tile = cluster; tile < num_tiles; tile += nclusters) {
+            for (int kb = 0; kb < nk; ++kb) {
+                ptx::mbar_wait(&fullP[sp], php);
+                const uint8_t* src = ringP + sp * Cfg::kStageP;
+                uint4 pk[kPer];
+#pragma unroll
+                for (int i = 0; i < kPer; ++i) {
+                    const int id = u + kUnpThreads * i;
+                    pk[i] = *reinterpret_cast<const uint4*>(src + (id >> 2) * 64 + (id & 3) * 16);
+                }
+                ptx::mbar_wait(&empty8[s8], ph8 ^ 1);
+                uint8_t* dst = ring8 + s8 * Cfg::kStage8;
+#pragma unroll
+                for (int i = 0; i < kPer; ++i) {
+                    const int id = u + kUnpThreads * i;
+                    const int r = id >> 2, c = id & 3;
+                    const uint4 pv = pk[i];
+                    uint4 lo, hi;
+                    lo.x = (pv.x << 4) & 0xF0F0F0F0u; hi.x = pv.x & 0xF0F0F0F0u;
+                    lo.y = (pv.y << 4) & 0xF0F0F0F0u; hi.y = pv.y & 0xF0F0F0F0u;
+                    lo.z = (pv.z << 4) & 0xF0F0F0F0u; hi.z = pv.z & 0xF0F0F0F0u;
+                    lo.w = (pv.w << 4) & 0xF0F0F0F0u; hi.w = pv.w & 0xF0F0F0F0u;
+                    const int r7 = r & 7;
+                    uint8_t* drow = dst + r * 128;
+                    *reinterpret_cast<uint4*>(drow + (((2 * c) ^ r7) << 4)) = lo;
+                    *reinterpret_cast<uint4*>(drow + (((2 * c + 1) ^ r7) << 4)) = hi;
+                }
+                // release the packed stage only after its data has been consumed
+                // (the STS above depend on the loaded registers): a generic-proxy
+                // release does not order pending LDS against the async-proxy TMA
+                // refill of the same bytes.
+                ptx::mbar_arrive(&emptyP[sp]);
+                ptx::fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&ready8[s8]);
+                if (++sp == SP) { sp = 0; php ^= 1; }
+                if (++s8 == S8) { s8 = 0; ph8 ^= 1; }
+            }
+        }
+    }
+
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    if (warp == 2) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc_2cta<Cfg::kTmemCols>(tmem_base);
+    }
+}
+
+}  // namespace mkq

@@ -8,6 +8,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -15,6 +16,8 @@
 #include "../../include/mkq.h"
 #include "attention.cuh"
 #include "gemm_sm100.cuh"
+#include "gemm2_sm100.cuh"
+#include "requant.cuh"
 #include "layernorm.cuh"
 #include "quantize.cuh"
 
@@ -89,15 +92,16 @@ EncodeTiledFn encode_fn() {
     return fn;
 }
 
-using MapKey = std::tuple<uintptr_t, uint64_t, uint64_t, uint64_t, uint32_t, uint32_t, int, int>;
+using MapKey = std::tuple<uintptr_t, uint64_t, uint64_t, uint64_t, uint32_t, uint32_t, int, int, int>;
 std::map<MapKey, CUtensorMap> g_maps;
 
-// 2-D uint8 map: inner extent `inner` bytes, `rows` rows, row stride `ld`.
-mkq_status make_map(CUtensorMap* out, const void* base, uint64_t inner, uint64_t rows, uint64_t ld,
-                    uint32_t box_inner, uint32_t box_rows, bool swz128) {
+// 2-D map over a row-major matrix: `inner` elements of `dtype` per row, `rows`
+// rows, row stride `ld` bytes; box {box_inner, box_rows}; swizzle mode.
+mkq_status make_map_t(CUtensorMap* out, const void* base, CUtensorMapDataType dtype, uint64_t inner, uint64_t rows,
+                      uint64_t ld, uint32_t box_inner, uint32_t box_rows, CUtensorMapSwizzle swz) {
     int dev = 0;
     cudaGetDevice(&dev);
-    MapKey key{reinterpret_cast<uintptr_t>(base), inner, rows, ld, box_inner, box_rows, swz128 ? 1 : 0, dev};
+    MapKey key{reinterpret_cast<uintptr_t>(base), inner, rows, ld, box_inner, box_rows, (int)swz, dev, (int)dtype};
     {
         std::lock_guard<std::mutex> lk(g_mu);
         auto it = g_maps.find(key);
@@ -112,15 +116,38 @@ mkq_status make_map(CUtensorMap* out, const void* base, uint64_t inner, uint64_t
     cuuint64_t strides[1] = {ld};
     cuuint32_t box[2] = {box_inner, box_rows};
     cuuint32_t es[2] = {1, 1};
-    CUresult r = fn(out, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, es,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE,
-                    swz128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+    CUresult r = fn(out, dtype, 2, const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(MKQ_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
     std::lock_guard<std::mutex> lk(g_mu);
     if (g_maps.size() > 4096) g_maps.clear();
     g_maps[key] = *out;
     return MKQ_OK;
+}
+
+mkq_status make_map(CUtensorMap* out, const void* base, uint64_t inner, uint64_t rows, uint64_t ld,
+                    uint32_t box_inner, uint32_t box_rows, bool swz128) {
+    return make_map_t(out, base, CU_TENSOR_MAP_DATA_TYPE_UINT8, inner, rows, ld, box_inner, box_rows,
+                      swz128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE);
+}
+
+// Output map of the 2-CTA epilogue: 32-column x 32-row blocks staged in
+// shared memory with the swizzle matching mkq::stg_off().
+mkq_status make_out_map(CUtensorMap* out, void* base, int mode, int64_t M, int64_t N, int64_t ldo) {
+    switch (mode) {
+    case MKQ_OUT_F32:
+        return make_map_t(out, base, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, N, M, ldo, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+    case MKQ_OUT_I32:
+        return make_map_t(out, base, CU_TENSOR_MAP_DATA_TYPE_INT32, N, M, ldo, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+    case MKQ_OUT_F16:
+        return make_map_t(out, base, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, N, M, ldo, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+    case MKQ_OUT_BF16:
+        return make_map_t(out, base, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, N, M, ldo, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+    case MKQ_OUT_I8:
+        return make_map_t(out, base, CU_TENSOR_MAP_DATA_TYPE_UINT8, N, M, ldo, 32, 32, CU_TENSOR_MAP_SWIZZLE_32B);
+    default:  // MKQ_OUT_I4: packed bytes
+        return make_map_t(out, base, CU_TENSOR_MAP_DATA_TYPE_UINT8, N / 2, M, ldo, 16, 32, CU_TENSOR_MAP_SWIZZLE_NONE);
+    }
 }
 
 // ------------------------------------------------------------------ GEMM dispatch
@@ -156,12 +183,42 @@ bool code_range_ok(int bits, int qmin, int qmax) {
     return qmin >= lo && qmax <= hi && qmin < qmax;
 }
 
+template <class Cfg>
+mkq_status launch_gemm2(const void* a, int64_t lda, const void* w, int64_t ldw, int M, int N, int K,
+                        const mkq::Epi2Params& ep, int sms, cudaStream_t st) {
+    static bool attr_set[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!attr_set[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(mkq::gemm_w4a4_2cta_kernel<Cfg>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+        attr_set[dev] = true;
+    }
+    CUtensorMap ma, mb;
+    mkq_status s = make_map(&ma, a, (uint64_t)K / 2, (uint64_t)M, (uint64_t)lda, Cfg::BK / 2, Cfg::BM, false);
+    if (s != MKQ_OK) return s;
+    s = make_map(&mb, w, (uint64_t)K / 2, (uint64_t)N, (uint64_t)ldw, Cfg::BK / 2, Cfg::BNH, false);
+    if (s != MKQ_OK) return s;
+    CUtensorMap mo;
+    s = make_out_map(&mo, ep.e.out, ep.e.mode, M, N, ep.e.ldo_bytes);
+    if (s != MKQ_OK) return s;
+    const int tiles = ((M + 2 * Cfg::BM - 1) / (2 * Cfg::BM)) * ((N + Cfg::BN - 1) / Cfg::BN);
+    static const int max_cl = [] { const char* v = getenv("MKQ_MAX_CLUSTERS"); return v ? atoi(v) : 0; }();
+    int clusters = tiles < sms / 2 ? tiles : sms / 2;
+    if (max_cl > 0 && clusters > max_cl) clusters = max_cl;
+    mkq::gemm_w4a4_2cta_kernel<Cfg><<<2 * clusters, Cfg::kThreads, Cfg::kSmem, st>>>(ma, mb, mo, ep, M, N, K);
+    cudaError_t e = cudaPeekAtLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "gemm2 launch");
+    return MKQ_OK;
+}
+
 mkq_status gemm_common(bool int4, const void* a, int64_t lda, const void* w, int64_t ldw, int64_t M, int64_t N,
                        int64_t K, float s_a, const float* s_w, const float* bias, const mkq_epilogue* epi, void* out,
                        int64_t ldo, void* ws, size_t ws_bytes, void* stream) {
     (void)ws;
     (void)ws_bytes;
-    mkq_epilogue e{MKQ_OUT_F32, 0, 1.0f, 0, 0};
+    mkq_epilogue e{MKQ_OUT_F32, 0, 1.0f, 0, 0, nullptr};
     if (epi) e = *epi;
     if (M < 0 || N < 0 || K < 0) return fail(MKQ_ERR_SHAPE, "negative dimension");
     if (M == 0) return MKQ_OK;
@@ -207,6 +264,18 @@ mkq_status gemm_common(bool int4, const void* a, int64_t lda, const void* w, int
     ep.ldo_bytes = ldo;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const bool wide = (N % 256 == 0) && (M > 128 * sms / 2 || (M / 128 + 1) * (N / 256) >= sms);
+    static const int path_override = [] {   // MKQ_GEMM_PATH=1cta|2cta (diagnostics)
+        const char* v = getenv("MKQ_GEMM_PATH");
+        return v ? (strcmp(v, "1cta") == 0 ? 1 : (strcmp(v, "2cta") == 0 ? 2 : 0)) : 0;
+    }();
+    const bool two_cta = path_override == 2 ? (N % 128 == 0) : (path_override == 1 ? false : (M > 128 && N % 128 == 0));
+    if (int4 && two_cta) {
+        mkq::Epi2Params p2{ep, (e.out == MKQ_OUT_I4 || e.out == MKQ_OUT_I8) ? e.requant_table : nullptr};
+        if (p2.table && !aligned16(p2.table)) return fail(MKQ_ERR_ALIGN, "requant_table must be 16-byte aligned");
+        if (N % 256 == 0)
+            return launch_gemm2<mkq::Gemm2Cfg<256>>(a, lda, w, ldw, (int)M, (int)N, (int)K, p2, sms, st);
+        return launch_gemm2<mkq::Gemm2Cfg<128>>(a, lda, w, ldw, (int)M, (int)N, (int)K, p2, sms, st);
+    }
     if (int4) {
         if (wide) return launch_gemm<mkq::GemmCfg<256, true>>(a, lda, w, ldw, (int)M, (int)N, (int)K, ep, sms, st);
         return launch_gemm<mkq::GemmCfg<128, true>>(a, lda, w, ldw, (int)M, (int)N, (int)K, ep, sms, st);
@@ -331,6 +400,70 @@ mkq_status mkq_gemm_w8a8(const void* a, int64_t lda, const void* w, int64_t ldw,
 }
 
 size_t mkq_gemm_workspace_size(int64_t, int64_t, int64_t) { return 0; }
+
+size_t mkq_requant_table_size(void) { return mkq::rq::kTableBytes; }
+
+}  // extern "C"
+
+namespace mkq {
+namespace rq {
+__global__ void init_kernel(Header* h, float y_lo, float y_hi, float inv_w, float y_zero, int ncell, int code_lo,
+                            int code_hi, int gelu, int qmin, int qmax, float s) {
+    Header v{};
+    v.y_lo = y_lo; v.y_hi = y_hi; v.inv_w = inv_w; v.y_zero = y_zero;
+    v.ncell = ncell; v.code_lo = code_lo; v.code_hi = code_hi; v.valid = 0;
+    v.gelu = gelu; v.qmin = qmin; v.qmax = qmax; v.nchg = 0; v.s_out = s;
+    *h = v;
+}
+}  // namespace rq
+}  // namespace mkq
+
+extern "C" {
+
+mkq_status mkq_requant_table(int gelu, float s_out, int qmin, int qmax, void* table, size_t table_bytes,
+                             void* stream) {
+    if (!table) return fail(MKQ_ERR_NULL, "table is required");
+    if (table_bytes < mkq::rq::kTableBytes) return fail(MKQ_ERR_WORKSPACE, "table needs %zu bytes", mkq::rq::kTableBytes);
+    if (!aligned16(table)) return fail(MKQ_ERR_ALIGN, "table must be 16-byte aligned");
+    if (!finite_pos(s_out) || s_out > 1e30f || s_out < 1e-30f) return fail(MKQ_ERR_SCALE, "s_out out of range");
+    if (gelu != 0 && gelu != 1) return fail(MKQ_ERR_RANGE, "gelu must be 0 or 1");
+    const int bits = (qmin >= -8 && qmax <= 7) ? 4 : 8;
+    if (!code_range_ok(bits, qmin, qmax) || qmin > 0 || qmax < 0) return fail(MKQ_ERR_RANGE, "need qmin <= 0 <= qmax");
+    int sms = 0;
+    mkq_status s = check_device(&sms);
+    if (s != MKQ_OK) return s;
+    using namespace mkq::rq;
+    float y_lo, y_hi;
+    int code_lo, code_hi = qmax;
+    if (gelu) {
+        y_lo = -5.6f;
+        y_hi = fmaxf(5.6f, (float)(qmax + 1) * s_out);
+        code_lo = 0;
+    } else {
+        y_lo = (float)(qmin - 1) * s_out;
+        y_hi = (float)(qmax + 1) * s_out;
+        code_lo = qmin;
+    }
+    const float y_zero = 0.49f * s_out;
+    if (!(y_lo < -y_zero && y_zero < y_hi)) return fail(MKQ_ERR_SCALE, "s_out too large for the table range");
+    const float inv_w = (float)kCells / (y_hi - y_lo);
+    uint32_t bz, bh, bl;
+    memcpy(&bz, &y_zero, 4);
+    memcpy(&bh, &y_hi, 4);
+    const float ny_lo = -y_lo;
+    memcpy(&bl, &ny_lo, 4);
+    const uint32_t np = bh - bz + 1, nn = bl - bz + 1;
+    Header* h = static_cast<Header*>(table);
+    uint2* cells = reinterpret_cast<uint2*>(h + 1);
+    Change* chg = reinterpret_cast<Change*>(static_cast<uint8_t*>(table) + sizeof(Header) + kCells * 8);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    init_kernel<<<1, 1, 0, st>>>(h, y_lo, y_hi, inv_w, y_zero, kCells, code_lo, code_hi, gelu, qmin, qmax, s_out);
+    scan_kernel<<<sms * 8, 256, 0, st>>>(h, chg, bz, np, bz, nn);
+    finalize_kernel<<<1, 32, 0, st>>>(h, cells, chg);
+    verify_kernel<<<sms * 8, 256, 0, st>>>(h, cells, bz, np, bz, nn);
+    cudaError_t e = cudaPeekAtLastError();
+    return e == cudaSuccess ? MKQ_OK : cuda_fail(e, "requant table launch");
+}
 
 mkq_status mkq_attention(const void* qkv, int64_t ld, int64_t batch, int64_t max_seq, const int32_t* cu,
                          int64_t tokens, int heads, int head_dim, int out_mode, float s_out, int qmin, int qmax,
@@ -487,21 +620,21 @@ mkq_status mkq_bert_layer(const mkq_layer* L, const float* h_in, int64_t batch, 
     // a1: quantize the layer input (per-tensor static scale, by value)
     MKQ_TRY(quantize_internal(h_in, T, h, h, nullptr, L->s_qkv_in, 0, bits, qlo, qhi, codes_in, cbh, sms, st));
     // a2-a4: QKV projection -> fp16 q|k|v (R10)
-    mkq_epilogue e_f16{MKQ_OUT_F16, 0, 1.0f, 0, 0};
+    mkq_epilogue e_f16{MKQ_OUT_F16, 0, 1.0f, 0, 0, nullptr};
     MKQ_TRY(gemm(codes_in, cbh, L->w_qkv, cbh, T, 3 * h, h, L->s_qkv_in, L->sw_qkv, L->b_qkv, &e_f16, qkv,
                  3 * h * 2, nullptr, 0, stream));
     // a8: attention core, fused quantize of OA with s_o_in
     MKQ_TRY(mkq_attention(qkv, 3 * h, batch, max_seq, cu, T, L->heads, 64, bits == 4 ? MKQ_OUT_I4 : MKQ_OUT_I8,
                           L->s_o_in, qlo, qhi, codes_oa, cbh, stream));
     // W^A projection (+ b^A) -> fp32
-    mkq_epilogue e_f32{MKQ_OUT_F32, 0, 1.0f, 0, 0};
+    mkq_epilogue e_f32{MKQ_OUT_F32, 0, 1.0f, 0, 0, nullptr};
     MKQ_TRY(gemm(codes_oa, cbh, L->w_o, cbh, T, h, h, L->s_o_in, L->sw_o, L->b_o, &e_f32, o, h * 4, nullptr, 0,
                  stream));
     // LN1(o + h) -> h1 fp32 and its codes for FFN1 (fused a1)
     MKQ_TRY(mkq_residual_layernorm(o, h_in, T, h, h, L->ln1_g, L->ln1_b, L->ln_eps, h1, bits, L->s_ffn1_in, qlo,
                                    qhi, codes_h1, cbh, stream));
     // FFN1: GELU + requantize to the FFN2 input codes (a5, a6 fused)
-    mkq_epilogue e_ffn1{bits == 4 ? MKQ_OUT_I4 : MKQ_OUT_I8, 1, L->s_ffn2_in, qlo, qhi};
+    mkq_epilogue e_ffn1{bits == 4 ? MKQ_OUT_I4 : MKQ_OUT_I8, 1, L->s_ffn2_in, qlo, qhi, L->ffn1_requant_table};
     MKQ_TRY(gemm(codes_h1, cbh, L->w_1, cbh, T, F, h, L->s_ffn1_in, L->sw_1, L->b_1, &e_ffn1, codes_ffn2, cbf,
                  nullptr, 0, stream));
     // FFN2 -> fp32

@@ -1,0 +1,164 @@
+// requant.cuh -- exact lookup table for the fused GELU + requantize epilogue
+// (§8a rows a5-a6; SURVEY §7.3-3 "epilogue ALU budget").
+//
+// The FFN1 epilogue maps y = fma((float)acc, sc[n], b[n]) to the FFN2 input
+// code  c(y) = clamp(rint_even(gelu_pinned(y) / s_out), qmin, qmax)  (R2-R7).
+// c depends on the fp32 value y only -- not on the column -- so one table in
+// y-space serves every column.  Evaluating gelu_pinned + an IEEE division per
+// output costs ~45 ALU ops, more than the tensor core leaves per output at
+// K = 1024; the table replaces them by a cell index, one shared-memory load
+// and one compare:
+//     cell i = floor((y - y_lo) * inv_w)               (same fp32 ops as here)
+//     c      = y >= thr[i] ? above[i] : below[i]       (exact fp32 compare)
+// Exactness is by construction, not by approximation: the builder evaluates
+// c(y) with the SAME device functions for EVERY fp32 y where c can change
+// (all floats in [y_lo, -y_zero] and [y_zero, y_hi]); outside those ranges c
+// is constant by proof (|gelu_pinned(y)| <= |y| gives c = 0 for |y| < 0.49 s;
+// gelu_pinned(y) = 0 for y <= -5.6 and = y for y >= 5.6).  A cell holding more
+// than one change point is flagged `direct` and evaluated with the full
+// pipeline.  A verify pass re-checks lookup == direct for every float of the
+// scanned ranges and clears `valid` on any mismatch (the epilogue then falls
+// back to direct evaluation); nothing here needs a host synchronization.
+#pragma once
+#include <cstdint>
+#include "epilogue.cuh"
+
+namespace mkq {
+namespace rq {
+
+constexpr int kCells = 1024;
+constexpr int kMaxChanges = 4096;
+
+struct Header {
+    float y_lo, y_hi, inv_w, y_zero;
+    int ncell, code_lo, code_hi, valid;
+    int gelu, qmin, qmax, nchg;
+    float s_out;
+    int pad[3];
+};   // 64 bytes
+
+struct Change {
+    float y;
+    int before, after, pad;
+};
+
+// table bytes: header + cells (uint2: thr bits, meta) + change scratch
+constexpr size_t kTableBytes = sizeof(Header) + kCells * 8 + kMaxChanges * sizeof(Change);
+constexpr size_t kSmemBytes = sizeof(Header) + kCells * 8;
+
+__device__ __forceinline__ int direct_code(float y, int gelu, float s, int qmin, int qmax) {
+    return quant_code(gelu ? gelu_pinned(y) : y, s, qmin, qmax);
+}
+
+__device__ __forceinline__ int cell_of(float y, float y_lo, float inv_w, int ncell) {
+    int i = __float2int_rd(__fmul_rn(__fsub_rn(y, y_lo), inv_w));
+    return min(max(i, 0), ncell - 1);
+}
+
+// meta: bits 0-7 code_below (int8), 8-15 code_above (int8), 16 direct
+__device__ __forceinline__ int lookup(const Header& h, const uint2* cells, float y) {
+    if (y < h.y_lo) return h.code_lo;
+    if (y >= h.y_hi) return h.code_hi;
+    const uint2 e = cells[cell_of(y, h.y_lo, h.inv_w, h.ncell)];
+    if (e.y & 0x10000u) return direct_code(y, h.gelu, h.s_out, h.qmin, h.qmax);
+    const int below = (int)(int8_t)(e.y & 0xFF), above = (int)(int8_t)((e.y >> 8) & 0xFF);
+    return y >= __uint_as_float(e.x) ? above : below;
+}
+
+__device__ __forceinline__ float next_down(float y) {   // largest float < y (y finite, != -0)
+    const uint32_t b = __float_as_uint(y);
+    if (y > 0.0f) return __uint_as_float(b - 1);
+    if (y == 0.0f) return -__uint_as_float(1u);
+    return __uint_as_float(b + 1);
+}
+
+// Range r in {0: positive [y_zero, y_hi], 1: negative [y_lo, -y_zero]} as a
+// run of consecutive floats in increasing y order: index k -> y.
+__device__ __forceinline__ float range_y(int r, uint32_t b0, uint32_t n, uint32_t k) {
+    // positive: bits b0..b0+n-1 ascending; negative: magnitudes from the top down
+    return r == 0 ? __uint_as_float(b0 + k) : -__uint_as_float(b0 + (n - 1 - k));
+}
+
+__global__ void scan_kernel(Header* h, Change* chg, uint32_t bp0, uint32_t np, uint32_t bn0, uint32_t nn) {
+    const uint32_t total = np + nn;
+    constexpr uint32_t kRun = 64;
+    const uint32_t runs = (total + kRun - 1) / kRun;
+    const int gelu = h->gelu, qmin = h->qmin, qmax = h->qmax;
+    const float s = h->s_out;
+    for (uint32_t run = blockIdx.x * blockDim.x + threadIdx.x; run < runs; run += gridDim.x * blockDim.x) {
+        const uint32_t k0 = run * kRun;
+        const uint32_t k1 = min(k0 + kRun, total);
+        // runs never straddle the two ranges: split at np
+        uint32_t k = k0;
+        while (k < k1) {
+            const int r = k < np ? 0 : 1;
+            const uint32_t kend = r == 0 ? min(k1, np) : k1;
+            const uint32_t b0 = r == 0 ? bp0 : bn0, n = r == 0 ? np : nn, kk0 = r == 0 ? k : k - np;
+            float y = range_y(r, b0, n, kk0);
+            int prev = direct_code(next_down(y), gelu, s, qmin, qmax);
+            for (uint32_t kk = kk0; kk < kk0 + (kend - k); ++kk) {
+                y = range_y(r, b0, n, kk);
+                const int c = direct_code(y, gelu, s, qmin, qmax);
+                if (c != prev) {
+                    const int i = atomicAdd(&h->nchg, 1);
+                    if (i < kMaxChanges) chg[i] = Change{y, prev, c, 0};
+                }
+                prev = c;
+            }
+            k = kend;
+        }
+    }
+}
+
+__device__ __forceinline__ uint32_t ord_key(float y) {   // monotone float -> uint
+    const uint32_t b = __float_as_uint(y);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+
+__global__ void finalize_kernel(Header* h, uint2* cells, Change* chg) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const int n = h->nchg;
+    if (n > kMaxChanges) { h->valid = 0; return; }
+    for (int i = 1; i < n; ++i) {   // insertion sort by y (n is small: <= ~300)
+        Change c = chg[i];
+        int j = i - 1;
+        while (j >= 0 && ord_key(chg[j].y) > ord_key(c.y)) { chg[j + 1] = chg[j]; --j; }
+        chg[j + 1] = c;
+    }
+    int run = h->code_lo;
+    int p = 0;
+    bool ok = true;
+    for (int i = 0; i < h->ncell; ++i) {
+        int cnt = 0;
+        float thr = 0.0f;
+        int below = run, above = run;
+        while (p < n && cell_of(chg[p].y, h->y_lo, h->inv_w, h->ncell) == i) {
+            if (cnt == 0) { thr = chg[p].y; if (chg[p].before != run) ok = false; }
+            run = chg[p].after;
+            above = run;
+            ++cnt;
+            ++p;
+        }
+        uint32_t meta = (uint32_t)(below & 0xFF) | ((uint32_t)(above & 0xFF) << 8) | (cnt > 1 ? 0x10000u : 0u);
+        const float t = cnt == 0 ? __int_as_float(0x7f800000) : thr;   // +inf: never reached
+        cells[i] = make_uint2(__float_as_uint(t), meta);
+    }
+    if (run != h->code_hi || p != n) ok = false;
+    h->valid = ok ? 1 : 0;
+}
+
+__global__ void verify_kernel(Header* h, const uint2* cells, uint32_t bp0, uint32_t np, uint32_t bn0, uint32_t nn) {
+    if (!h->valid) return;
+    const Header hh = *h;
+    const uint32_t total = np + nn;
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < total; k += gridDim.x * blockDim.x) {
+        const float y = k < np ? range_y(0, bp0, np, k) : range_y(1, bn0, nn, k - np);
+        if (lookup(hh, cells, y) != direct_code(y, hh.gelu, hh.s_out, hh.qmin, hh.qmax)) {
+            h->valid = 0;
+            return;
+        }
+    }
+}
+
+}  // namespace rq
+}  // namespace mkq

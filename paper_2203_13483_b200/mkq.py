@@ -13,7 +13,7 @@ import torch
 from ._lib import (OUT_BF16, OUT_F16, OUT_F32, OUT_I32, OUT_I4, OUT_I8, MkqEpilogue, MkqLayer,
                    check, lib)
 
-__all__ = ["mkq_quantize_pack", "mkq_absmax_scale", "mkq_gemm_w4a4", "mkq_gemm_w8a8",
+__all__ = ["mkq_requant_table", "mkq_quantize_pack", "mkq_absmax_scale", "mkq_gemm_w4a4", "mkq_gemm_w8a8",
            "mkq_attention", "mkq_residual_layernorm", "mkq_bert_layer", "out_dtype_bytes",
            "OUT_F32", "OUT_BF16", "OUT_I32", "OUT_I4", "OUT_I8", "OUT_F16"]
 
@@ -66,13 +66,39 @@ def mkq_absmax_scale(x: torch.Tensor, l_max: float, per_row: bool = True, out: O
     return out
 
 
+_TABLES = {}
+
+
+def mkq_requant_table(gelu: bool, s_out: float, qmin: int, qmax: int, device=None, stream=None,
+                      cache: bool = True) -> torch.Tensor:
+    """Exact y-space lookup table of the fused (GELU +) requantize epilogue,
+    built on the device by libmkq (mkq_requant_table)."""
+    device = torch.device(device if device is not None else "cuda")
+    if device.index is None:
+        device = torch.device("cuda", torch.cuda.current_device())
+    key = (bool(gelu), float(s_out), int(qmin), int(qmax), str(device))
+    if cache and key in _TABLES:
+        return _TABLES[key]
+    nbytes = int(lib().mkq_requant_table_size())
+    t = torch.empty(nbytes, dtype=torch.uint8, device=device)
+    check("mkq_requant_table", lib().mkq_requant_table(int(gelu), float(s_out), qmin, qmax, _ptr(t), nbytes,
+                                                       _stream(stream)))
+    if cache:
+        _TABLES[key] = t
+    return t
+
+
 def _gemm(name: str, a, w, K: int, s_a: float, s_w, bias, mode: int, gelu: bool, s_out: float, qmin: int,
-          qmax: int, out, stream):
+          qmax: int, out, stream, requant_table=None):
     M, N = a.shape[0], w.shape[0]
     if out is None:
         dt, nb = out_dtype_bytes(mode)
         out = torch.empty((M, int(N * nb) if mode == OUT_I4 else N), dtype=dt, device=a.device)
-    epi = MkqEpilogue(mode, int(gelu), float(s_out), qmin, qmax)
+    if isinstance(requant_table, bool):
+        requant_table = mkq_requant_table(gelu, s_out, qmin, qmax, a.device, stream) \
+            if (requant_table and mode in (OUT_I4, OUT_I8)) else None
+    epi = MkqEpilogue(mode, int(gelu), float(s_out), qmin, qmax,
+                      None if requant_table is None else requant_table.data_ptr())
     fn = getattr(lib(), name)
     check(name, fn(_ptr(a), _row_bytes(a), _ptr(w), _row_bytes(w), M, N, K, float(s_a), _ptr(s_w), _ptr(bias),
                    ctypes.byref(epi), _ptr(out), _row_bytes(out), None, 0, _stream(stream)))
@@ -82,19 +108,23 @@ def _gemm(name: str, a, w, K: int, s_a: float, s_w, bias, mode: int, gelu: bool,
 def mkq_gemm_w4a4(a: torch.Tensor, w: torch.Tensor, s_a: float, s_w: torch.Tensor,
                   bias: Optional[torch.Tensor] = None, mode: int = OUT_F32, gelu: bool = False,
                   s_out: float = 1.0, qmin: int = -8, qmax: int = 7, out: Optional[torch.Tensor] = None,
-                  K: Optional[int] = None, stream=None) -> torch.Tensor:
-    """W4A4 linear (§8a-a2..a6): a packed [M, K/2], w packed [N, K/2]."""
+                  K: Optional[int] = None, stream=None, requant_table=True) -> torch.Tensor:
+    """W4A4 linear (§8a-a2..a6): a packed [M, K/2], w packed [N, K/2].
+    requant_table: True = build/cache the exact requant table (I4/I8 modes),
+    False/None = direct evaluation, or a prebuilt table tensor."""
     K = K if K is not None else a.shape[1] * 2
-    return _gemm("mkq_gemm_w4a4", a, w, K, s_a, s_w, bias, mode, gelu, s_out, qmin, qmax, out, stream)
+    return _gemm("mkq_gemm_w4a4", a, w, K, s_a, s_w, bias, mode, gelu, s_out, qmin, qmax, out, stream,
+                 requant_table)
 
 
 def mkq_gemm_w8a8(a: torch.Tensor, w: torch.Tensor, s_a: float, s_w: torch.Tensor,
                   bias: Optional[torch.Tensor] = None, mode: int = OUT_F32, gelu: bool = False,
                   s_out: float = 1.0, qmin: int = -128, qmax: int = 127, out: Optional[torch.Tensor] = None,
-                  K: Optional[int] = None, stream=None) -> torch.Tensor:
+                  K: Optional[int] = None, stream=None, requant_table=True) -> torch.Tensor:
     """W8A8 linear (§8a-a7): a int8 [M, K], w int8 [N, K]."""
     K = K if K is not None else a.shape[1]
-    return _gemm("mkq_gemm_w8a8", a, w, K, s_a, s_w, bias, mode, gelu, s_out, qmin, qmax, out, stream)
+    return _gemm("mkq_gemm_w8a8", a, w, K, s_a, s_w, bias, mode, gelu, s_out, qmin, qmax, out, stream,
+                 requant_table)
 
 
 def mkq_attention(qkv: torch.Tensor, heads: int, batch: int, max_seq: int,
@@ -139,14 +169,18 @@ class QLayer:
               "ln1_g", "ln1_b", "ln2_g", "ln2_b")
 
     def __init__(self, hidden: int, heads: int, ffn: int, bits: int, tensors: dict, scales: dict,
-                 ln_eps: float = 1e-12):
+                 ln_eps: float = 1e-12, use_table: bool = True):
         self.hidden, self.heads, self.ffn, self.bits = hidden, heads, ffn, bits
         self.t = {k: tensors[k].contiguous() for k in self.FIELDS}
         self.scales = {k: float(scales[k]) for k in ("s_qkv_in", "s_o_in", "s_ffn1_in", "s_ffn2_in")}
         self.ln_eps = ln_eps
+        lo, hi = (-8, 7) if bits == 4 else (-128, 127)
+        dev = self.t["w_qkv"].device
+        self.table = mkq_requant_table(True, self.scales["s_ffn2_in"], lo, hi, dev) if use_table else None
         self.c = MkqLayer(hidden, heads, ffn, bits, *[self.t[k].data_ptr() for k in self.FIELDS],
                           self.scales["s_qkv_in"], self.scales["s_o_in"], self.scales["s_ffn1_in"],
-                          self.scales["s_ffn2_in"], float(ln_eps))
+                          self.scales["s_ffn2_in"], float(ln_eps),
+                          None if self.table is None else self.table.data_ptr())
 
     def workspace_size(self, tokens: int) -> int:
         return int(lib().mkq_bert_layer_workspace_size(ctypes.byref(self.c), tokens))

@@ -84,7 +84,7 @@ def calibrate(layer: M.QLayer, h: torch.Tensor, batch: int, max_seq: int,
     c = M.mkq_quantize_pack(h1, torch.tensor([s["s_ffn1_in"]], device=h.device), bits, lo, hi)
     g = gemm(c, t["w_1"], s["s_ffn1_in"], t["sw_1"], t["b_1"], mode=M.OUT_F32, gelu=True, K=hd)
     s["s_ffn2_in"] = act_scale(g, hi)
-    rebuilt = M.QLayer(hd, layer.heads, F, bits, layer.t, s, layer.ln_eps)
+    rebuilt = M.QLayer(hd, layer.heads, F, bits, layer.t, s, layer.ln_eps, use_table=layer.table is not None)
     layer.__dict__.update(rebuilt.__dict__)
     return s
 

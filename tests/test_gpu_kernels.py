@@ -234,3 +234,39 @@ def test_device_errors_surface():
         M.mkq_gemm_w4a4(torch.zeros((4, 16), dtype=torch.uint8, device=DEV),
                         torch.zeros((33, 16), dtype=torch.uint8, device=DEV), 1.0,
                         torch.ones(33, device=DEV))
+
+
+# ------------------------------------------------------------------ requant table (a5/a6 fused)
+@pytest.mark.parametrize("gelu,s_out,bits", [(True, 0.05, 4), (True, 0.6, 4), (True, 3.0, 4), (False, 0.3, 4),
+                                             (True, 0.004, 8), (True, 0.04, 8), (False, 0.01, 8)])
+def test_requant_table_bitexact(gelu, s_out, bits):
+    lo, hi = (-8, 7) if bits == 4 else (-128, 127)
+    tab = M.mkq_requant_table(gelu, s_out, lo, hi, DEV, cache=False)
+    torch.cuda.synchronize()
+    assert int(tab[28:32].view(torch.int32).item()) == 1, "table self-verification failed"
+    rng = np.random.default_rng(int(s_out * 1000) + bits)
+    Mm, N, K = 1000, 1024, 1024
+    A, W = _codes(rng, Mm, N, K, bits)
+    s_a = np.float32(0.31 if bits == 4 else 0.02)
+    s_w = rng.uniform(1e-3, 5e-3, N).astype(np.float32) if bits == 4 else rng.uniform(1e-4, 3e-4, N).astype(np.float32)
+    b = rng.uniform(-0.1, 0.1, N).astype(np.float32)
+    mode = M.OUT_I4 if bits == 4 else M.OUT_I8
+    with_t = host(_run(bits, A, W, s_a, s_w, b, mode=mode, gelu=gelu, s_out=s_out, qmin=lo, qmax=hi,
+                       requant_table=tab))
+    without = host(_run(bits, A, W, s_a, s_w, b, mode=mode, gelu=gelu, s_out=s_out, qmin=lo, qmax=hi,
+                        requant_table=None))
+    assert np.array_equal(with_t, without)
+    ref = oracle.linear(A, W, s_a, s_w, b, mode=oracle.OUT_I4 if bits == 4 else oracle.OUT_I8, gelu=gelu,
+                        s_out=np.float32(s_out), qmin_out=lo, qmax_out=hi)
+    assert np.array_equal(with_t if bits == 4 else with_t.view(np.int8), oracle.pack_int4(ref) if bits == 4 else ref)
+
+
+def test_requant_table_mismatched_params_ignored():
+    """A table built for other (gelu, s_out, range) must not be used."""
+    tab = M.mkq_requant_table(True, 0.5, -8, 7, DEV, cache=False)
+    rng = np.random.default_rng(3)
+    A, W = _codes(rng, 512, 512, 512, 4)
+    s_w = rng.uniform(1e-3, 5e-3, 512).astype(np.float32)
+    out = host(_run(4, A, W, 0.3, s_w, None, mode=M.OUT_I4, gelu=True, s_out=0.07, requant_table=tab))
+    ref = oracle.linear(A, W, np.float32(0.3), s_w, None, mode=oracle.OUT_I4, gelu=True, s_out=np.float32(0.07))
+    assert np.array_equal(out, oracle.pack_int4(ref))
