@@ -17,8 +17,10 @@
 //   * double-buffered TMEM accumulators (2 x BN columns per CTA) so the
 //     epilogue of tile i overlaps the mainloop of tile i+1.
 // Barriers that gate the MMA (int8 stage full, accumulator empty) live in the
-// leader CTA (rank 0) and collect arrivals from both CTAs; MMA completion is
-// multicast to both CTAs' barriers.
+// leader CTA (rank 0) and collect one arrival per warp from both CTAs
+// (fence.proxy.async + CTA-scope remote mbarrier arrive, as CUTLASS's 2-SM
+// transform pipeline does; a cluster-scope release would be a GPU-scope
+// membar); MMA completion is multicast to both CTAs' barriers.
 #pragma once
 #include <cstdint>
 #include <cuda.h>
@@ -54,7 +56,7 @@ struct Gemm2Cfg {
     static constexpr uint32_t kTmemCols = 2 * BN;
     static constexpr int kScb = 2 * BN * 8;          // 2 buffers x BN x (sc, b)
     static constexpr int kStaging = kEpiWarps * 4096; // 32 rows x 128 B output block per warp
-    static constexpr int kBarBytes = 8 * (3 * S8 + 2 * SP + 6) + 16;
+    static constexpr int kBarBytes = 8 * (2 * S8 + 2 * SP + 4) + 16;
     static constexpr int kSmem = 1024 + S8 * kStage8 + SP * kStageP + (int)rq::kSmemBytes + kScb + kStaging + kBarBytes;
     static_assert(kSmem <= 232448, "shared memory budget");
     static_assert(BN == 256 || BN == 128, "BN");
@@ -66,7 +68,7 @@ struct Gemm2Cfg {
 // y >= y_hi need no special case: cell 0's "below" code is code_lo and the
 // last cell's "above" code is code_hi.
 struct Lut {
-    float y_lo, inv_w;
+    float c0, inv_w;  // cell = floor(fma(y, inv_w, c0)), c0 = -y_lo*inv_w (rq::cell_of)
     int ncell;
     uint32_t cells;   // shared-window address of cell 0
 };
@@ -91,7 +93,7 @@ __device__ __forceinline__ void lut_codes16(const Lut& L, const EpiParams& ep, c
     uint32_t dmask = 0;
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
-        const uint2 e = lds64(L.cells + 8u * (uint32_t)rq::cell_of(y[i], L.y_lo, L.inv_w, L.ncell));
+        const uint2 e = lds64(L.cells + 8u * (uint32_t)rq::cell_of(y[i], L.c0, L.inv_w, L.ncell));
         q[i] = y[i] >= __uint_as_float(e.x) ? (e.y >> 8) : e.y;
         dmask |= (e.y >> 16 & 1u) << i;
     }
@@ -150,8 +152,8 @@ __device__ __forceinline__ void epi2_half(const EpiParams& ep, const Lut& L, boo
             uint32_t a = 0, b = 0;
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-                a |= (q[i] & 0xFu) << (4 * i);
-                b |= (q[8 + i] & 0xFu) << (4 * i);
+                a += (q[i] & 0xFu) * (1u << (4 * i));
+                b += (q[8 + i] & 0xFu) * (1u << (4 * i));
             }
             *reinterpret_cast<uint2*>(stage + r * 16 + h2 * 8) = make_uint2(a, b);
         } else {
@@ -205,9 +207,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
     uint64_t* emptyP = fullP + SP;
     uint64_t* tfull = emptyP + SP;
     uint64_t* tempty = tfull + 2;
-    uint64_t* ready8 = tempty + 2;   // local: unpack warps -> relay
-    uint64_t* tdone = ready8 + S8;   // local: epilogue warps -> relay
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tdone + 2);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
     const EpiParams& ep = p.e;
     const int warp = threadIdx.x >> 5;
@@ -222,9 +222,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < S8; ++i) {
-            ptx::mbar_init(&full8[i], 2);                 // one relay arrive per CTA
+            ptx::mbar_init(&full8[i], 2 * Cfg::kUnpWarps);   // one arrive per unpack warp of each CTA
             ptx::mbar_init(&empty8[i], 1);
-            ptx::mbar_init(&ready8[i], Cfg::kUnpWarps);
+
         }
         for (int i = 0; i < SP; ++i) {
             ptx::mbar_init(&fullP[i], 1);
@@ -232,8 +232,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
         }
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(&tfull[i], 1);
-            ptx::mbar_init(&tempty[i], 2);
-            ptx::mbar_init(&tdone[i], Cfg::kEpiWarps);
+            ptx::mbar_init(&tempty[i], 2 * Cfg::kEpiWarps);
+
         }
         ptx::fence_barrier_init();
     }
@@ -293,33 +293,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
                 ptx::mma_commit_2cta_mc(&tfull[ab], 3);
             }
         }
-    } else if (warp == 3) {
-        // ---------------------------------------------------- relay: unpack -> leader
-        // Local (CTA-scope) arrivals of the 8 unpack warps are forwarded to the
-        // leader's full barrier with ONE cluster-scope release per stage (a
-        // cluster-scope release is a GPU-scope membar in SASS).
-        if (lane == 0) {
-            int s8 = 0;
-            uint32_t ph8 = 0;
-            for (int tile = cluster; tile < num_tiles; tile += nclusters)
-                for (int kb = 0; kb < nk; ++kb) {
-                    ptx::mbar_wait(&ready8[s8], ph8);
-                    ptx::mbar_arrive_cluster(ptx::mapa(&full8[s8], 0));
-                    if (++s8 == S8) { s8 = 0; ph8 ^= 1; }
-                }
-        }
-    } else if (warp == 2) {
-        // ---------------------------------------------------- relay: epilogue -> leader
-        if (lane == 0) {
-            int it = 0;
-            for (int tile = cluster; tile < num_tiles; tile += nclusters, ++it) {
-                const int ab = it & 1;
-                ptx::mbar_wait(&tdone[ab], (it >> 1) & 1);
-                ptx::tc_fence_after();
-                ptx::tc_fence_before();
-                ptx::mbar_arrive_cluster(ptx::mapa(&tempty[ab], 0));
-            }
-        }
     } else if (warp >= 4 && warp < 4 + Cfg::kEpiWarps) {
         // ---------------------------------------------------- epilogue (both CTAs)
         const int e = warp - 4;           // 0..7
@@ -337,7 +310,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
             use_table = th->valid != 0 && th->gelu == ep.gelu && th->s_out == ep.s_out && th->qmin == ep.qmin &&
                         th->qmax == ep.qmax;
         Lut L{0.0f, 0.0f, 1, ptx::smem_u32(tcells)};
-        if (use_table) L = Lut{th->y_lo, th->inv_w, th->ncell, ptx::smem_u32(tcells)};
+        if (use_table) L = Lut{th->c0, th->inv_w, th->ncell, ptx::smem_u32(tcells)};
         uint8_t* stage = staging + e * 4096;
         if (lane == 0) ptx::tma_prefetch_desc(&tmO);
         int it = 0;
@@ -380,7 +353,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
             }
             ptx::tc_fence_before();
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&tdone[ab]);
+            if (lane == 0) ptx::mbar_arrive_remote(ptx::mapa(&tempty[ab], 0));
         }
         if (lane == 0) ptx::tma_store_wait<0>();
     } else if (warp >= 4 + Cfg::kEpiWarps) {
@@ -388,36 +361,43 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
         const int u = threadIdx.x - 32 * (4 + Cfg::kEpiWarps);
         constexpr int kChunks = (BM + BNH) * (Cfg::BK / 32);   // 16-byte packed chunks per stage
         constexpr int kPer = kChunks / kUnpThreads;
-        static_assert(kChunks % kUnpThreads == 0, "chunk split");
+        static_assert(kChunks % kUnpThreads == 0 && kUnpThreads == 256, "chunk split: 64 rows per pass");
+        // Thread u always handles 16-byte chunk c = u & 3 of rows r = (u >> 2) + 64 i:
+        // its swizzle phase (r & 7) and both destination offsets are loop invariants.
+        const uint32_t r0 = (uint32_t)u >> 2, c = (uint32_t)u & 3u, r7 = r0 & 7u;
+        const uint32_t src_off = r0 * 64u + c * 16u;
+        const uint32_t dlo_off = r0 * 128u + (((2u * c) ^ r7) << 4);
+        const uint32_t dhi_off = r0 * 128u + (((2u * c + 1u) ^ r7) << 4);
+        const uint32_t ringP_s = ptx::smem_u32(ringP), ring8_s = ptx::smem_u32(ring8);
         int sp = 0, s8 = 0;
         uint32_t php = 0, ph8 = 0;
         for (int tile = cluster; tile < num_tiles; tile += nclusters) {
             for (int kb = 0; kb < nk; ++kb) {
                 ptx::mbar_wait(&fullP[sp], php);
-                const uint8_t* src = ringP + sp * Cfg::kStageP;
+                const uint32_t src = ringP_s + (uint32_t)sp * Cfg::kStageP + src_off;
                 uint4 pk[kPer];
+#ifndef MKQ_DBG_NO_UNPACK
 #pragma unroll
-                for (int i = 0; i < kPer; ++i) {
-                    const int id = u + kUnpThreads * i;
-                    pk[i] = *reinterpret_cast<const uint4*>(src + (id >> 2) * 64 + (id & 3) * 16);
-                }
+                for (int i = 0; i < kPer; ++i) pk[i] = ptx::lds128(src + (uint32_t)i * (64u * 64u));
+#endif
                 ptx::mbar_wait(&empty8[s8], ph8 ^ 1);
-                uint8_t* dst = ring8 + s8 * Cfg::kStage8;
+                const uint32_t dst = ring8_s + (uint32_t)s8 * Cfg::kStage8;
+#ifndef MKQ_DBG_NO_UNPACK
 #pragma unroll
                 for (int i = 0; i < kPer; ++i) {
-                    const int id = u + kUnpThreads * i;
-                    const int r = id >> 2, c = id & 3;
                     const uint4 pv = pk[i];
                     uint4 lo, hi;
-                    lo.x = (pv.x << 4) & 0xF0F0F0F0u; hi.x = pv.x & 0xF0F0F0F0u;
-                    lo.y = (pv.y << 4) & 0xF0F0F0F0u; hi.y = pv.y & 0xF0F0F0F0u;
-                    lo.z = (pv.z << 4) & 0xF0F0F0F0u; hi.z = pv.z & 0xF0F0F0F0u;
-                    lo.w = (pv.w << 4) & 0xF0F0F0F0u; hi.w = pv.w & 0xF0F0F0F0u;
-                    const int r7 = r & 7;
-                    uint8_t* drow = dst + r * 128;
-                    *reinterpret_cast<uint4*>(drow + (((2 * c) ^ r7) << 4)) = lo;
-                    *reinterpret_cast<uint4*>(drow + (((2 * c + 1) ^ r7) << 4)) = hi;
+                    lo.x = (pv.x * 16u) & 0xF0F0F0F0u; hi.x = pv.x & 0xF0F0F0F0u;
+                    lo.y = (pv.y * 16u) & 0xF0F0F0F0u; hi.y = pv.y & 0xF0F0F0F0u;
+                    lo.z = (pv.z * 16u) & 0xF0F0F0F0u; hi.z = pv.z & 0xF0F0F0F0u;
+                    lo.w = (pv.w * 16u) & 0xF0F0F0F0u; hi.w = pv.w & 0xF0F0F0F0u;
+                    const uint32_t rb = dst + (uint32_t)i * (64u * 128u);
+                    ptx::sts128(rb + dlo_off, lo);
+                    ptx::sts128(rb + dhi_off, hi);
                 }
+#else
+                (void)src; (void)dst; (void)pk;
+#endif
                 // release the packed stage only after its data has been consumed
                 // (the STS above depend on the loaded registers): a generic-proxy
                 // release does not order pending LDS against the async-proxy TMA
@@ -425,7 +405,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
                 ptx::mbar_arrive(&emptyP[sp]);
                 ptx::fence_proxy_async_smem();
                 __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(&ready8[s8]);
+                if (lane == 0) ptx::mbar_arrive_remote(ptx::mapa(&full8[s8], 0));
                 if (++sp == SP) { sp = 0; php ^= 1; }
                 if (++s8 == S8) { s8 = 0; ph8 ^= 1; }
             }

@@ -411,6 +411,7 @@ __global__ void init_kernel(Header* h, float y_lo, float y_hi, float inv_w, floa
                             int code_hi, int gelu, int qmin, int qmax, float s) {
     Header v{};
     v.y_lo = y_lo; v.y_hi = y_hi; v.inv_w = inv_w; v.y_zero = y_zero;
+    v.c0 = __fmul_rn(-y_lo, inv_w);
     v.ncell = ncell; v.code_lo = code_lo; v.code_hi = code_hi; v.valid = 0;
     v.gelu = gelu; v.qmin = qmin; v.qmax = qmax; v.nchg = 0; v.s_out = s;
     *h = v;

@@ -8,7 +8,7 @@
 // output costs ~45 ALU ops, more than the tensor core leaves per output at
 // K = 1024; the table replaces them by a cell index, one shared-memory load
 // and one compare:
-//     cell i = floor((y - y_lo) * inv_w)               (same fp32 ops as here)
+//     cell i = clamp(floor(fma(y, inv_w, c0)))          (same fp32 ops as here)
 //     c      = y >= thr[i] ? above[i] : below[i]       (exact fp32 compare)
 // Exactness is by construction, not by approximation: the builder evaluates
 // c(y) with the SAME device functions for EVERY fp32 y where c can change
@@ -30,11 +30,12 @@ constexpr int kCells = 1024;
 constexpr int kMaxChanges = 4096;
 
 struct Header {
-    float y_lo, y_hi, inv_w, y_zero;
+    float c0, y_hi, inv_w, y_zero;   // c0 = fl(-y_lo * inv_w)
     int ncell, code_lo, code_hi, valid;
     int gelu, qmin, qmax, nchg;
     float s_out;
-    int pad[3];
+    float y_lo;
+    int pad[2];
 };   // 64 bytes
 
 struct Change {
@@ -50,16 +51,18 @@ __device__ __forceinline__ int direct_code(float y, int gelu, float s, int qmin,
     return quant_code(gelu ? gelu_pinned(y) : y, s, qmin, qmax);
 }
 
-__device__ __forceinline__ int cell_of(float y, float y_lo, float inv_w, int ncell) {
-    int i = __float2int_rd(__fmul_rn(__fsub_rn(y, y_lo), inv_w));
+// cell index: floor(fma(y, inv_w, c0)) clamped; monotone non-decreasing in y
+// (RN of a monotone real function), identical on the build and lookup sides.
+__device__ __forceinline__ int cell_of(float y, float c0, float inv_w, int ncell) {
+    int i = __float2int_rd(__fmaf_rn(y, inv_w, c0));
     return min(max(i, 0), ncell - 1);
 }
 
-// meta: bits 0-7 code_below (int8), 8-15 code_above (int8), 16 direct
+// meta: bits 0-7 code_below (int8), 8-15 code_above (int8), 16 direct.
+// Exactly the epilogue's lookup: no range tests -- cells clamp, cell 0's
+// "below" is code_lo and every cell past the last change point holds code_hi.
 __device__ __forceinline__ int lookup(const Header& h, const uint2* cells, float y) {
-    if (y < h.y_lo) return h.code_lo;
-    if (y >= h.y_hi) return h.code_hi;
-    const uint2 e = cells[cell_of(y, h.y_lo, h.inv_w, h.ncell)];
+    const uint2 e = cells[cell_of(y, h.c0, h.inv_w, h.ncell)];
     if (e.y & 0x10000u) return direct_code(y, h.gelu, h.s_out, h.qmin, h.qmax);
     const int below = (int)(int8_t)(e.y & 0xFF), above = (int)(int8_t)((e.y >> 8) & 0xFF);
     return y >= __uint_as_float(e.x) ? above : below;
@@ -132,7 +135,7 @@ __global__ void finalize_kernel(Header* h, uint2* cells, Change* chg) {
         int cnt = 0;
         float thr = 0.0f;
         int below = run, above = run;
-        while (p < n && cell_of(chg[p].y, h->y_lo, h->inv_w, h->ncell) == i) {
+        while (p < n && cell_of(chg[p].y, h->c0, h->inv_w, h->ncell) == i) {
             if (cnt == 0) { thr = chg[p].y; if (chg[p].before != run) ok = false; }
             run = chg[p].after;
             above = run;
