@@ -89,18 +89,22 @@ __device__ __forceinline__ float4 lds128f(uint32_t addr) {
 }
 
 // 16 requantized codes (low byte of each q[i] is the two's-complement code).
+// 16 requantized codes as packed fields (int4 table: nibble 0..15; int8: byte)
 __device__ __forceinline__ void lut_codes16(const Lut& L, const EpiParams& ep, const float (&y)[16], uint32_t (&q)[16]) {
-    uint32_t dmask = 0;
+    uint32_t any = 0;
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
-        const uint2 e = lds64(L.cells + 8u * (uint32_t)rq::cell_of(y[i], L.c0, L.inv_w, L.ncell));
-        q[i] = y[i] >= __uint_as_float(e.x) ? (e.y >> 8) : e.y;
-        dmask |= (e.y >> 16 & 1u) << i;
+        const uint2 e = lds64(L.cells + 8u * rq::cell_u(y[i], L.c0, L.inv_w, (uint32_t)L.ncell));
+        q[i] = __byte_perm(e.y, 0, y[i] >= __uint_as_float(e.x) ? 0x4441 : 0x4440);
+        any |= e.y;
     }
-    if (__builtin_expect(__any_sync(0xffffffffu, dmask != 0), 0)) {
+    if (__builtin_expect(__any_sync(0xffffffffu, (any & 0x10000u) != 0), 0)) {
+        const uint32_t fm = ep.mode == OUT_I4 ? 0xFu : 0xFFu;
 #pragma unroll
-        for (int i = 0; i < 16; ++i)
-            if (dmask >> i & 1u) q[i] = (uint32_t)requant_direct(y[i], ep.gelu, ep.s_out, ep.qmin, ep.qmax);
+        for (int i = 0; i < 16; ++i) {
+            const uint32_t e = lds64(L.cells + 8u * rq::cell_u(y[i], L.c0, L.inv_w, (uint32_t)L.ncell)).y;
+            if (e & 0x10000u) q[i] = (uint32_t)requant_direct(y[i], ep.gelu, ep.s_out, ep.qmin, ep.qmax) & fm;
+        }
     }
 }
 
@@ -149,11 +153,15 @@ __device__ __forceinline__ void epi2_half(const EpiParams& ep, const Lut& L, boo
                 q[i] = (uint32_t)quant_code(ep.gelu ? gelu_pinned(y[i]) : y[i], ep.s_out, ep.qmin, ep.qmax);
         }
         if (mode == OUT_I4) {
+            if (!use_table) {   // table fields are already masked nibbles
+#pragma unroll
+                for (int i = 0; i < 16; ++i) q[i] &= 0xFu;
+            }
             uint32_t a = 0, b = 0;
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-                a += (q[i] & 0xFu) * (1u << (4 * i));
-                b += (q[8 + i] & 0xFu) * (1u << (4 * i));
+                a += q[i] * (1u << (4 * i));
+                b += q[8 + i] * (1u << (4 * i));
             }
             *reinterpret_cast<uint2*>(stage + r * 16 + h2 * 8) = make_uint2(a, b);
         } else {

@@ -58,14 +58,31 @@ __device__ __forceinline__ int cell_of(float y, float c0, float inv_w, int ncell
     return min(max(i, 0), ncell - 1);
 }
 
-// meta: bits 0-7 code_below (int8), 8-15 code_above (int8), 16 direct.
+// meta: byte 0 code_below, byte 1 code_above, bit 16 direct.  Codes are
+// stored as the output's packed field: a 4-bit nibble (0..15, the int4 two's
+// complement) for int4 tables (qmin >= -8, qmax <= 7), a byte otherwise, so
+// the epilogue selects one with a single PRMT and packs without masking.
+__device__ __forceinline__ bool is_int4(int qmin, int qmax) { return qmin >= -8 && qmax <= 7; }
+
+__device__ __forceinline__ int decode_field(uint32_t f, bool int4) {
+    return int4 ? (int)(f & 0xF) - (int)((f & 0x8) << 1) : (int)(int8_t)(f & 0xFF);
+}
+
+// cell index with an unsigned saturating conversion (negatives -> 0) and one
+// min: the epilogue's exact sequence
+__device__ __forceinline__ uint32_t cell_u(float y, float c0, float inv_w, uint32_t ncell) {
+    uint32_t i;
+    asm("cvt.rmi.u32.f32 %0, %1;" : "=r"(i) : "f"(__fmaf_rn(y, inv_w, c0)));
+    return min(i, ncell - 1u);
+}
+
 // Exactly the epilogue's lookup: no range tests -- cells clamp, cell 0's
 // "below" is code_lo and every cell past the last change point holds code_hi.
 __device__ __forceinline__ int lookup(const Header& h, const uint2* cells, float y) {
-    const uint2 e = cells[cell_of(y, h.c0, h.inv_w, h.ncell)];
+    const uint2 e = cells[cell_u(y, h.c0, h.inv_w, (uint32_t)h.ncell)];
     if (e.y & 0x10000u) return direct_code(y, h.gelu, h.s_out, h.qmin, h.qmax);
-    const int below = (int)(int8_t)(e.y & 0xFF), above = (int)(int8_t)((e.y >> 8) & 0xFF);
-    return y >= __uint_as_float(e.x) ? above : below;
+    const uint32_t f = __byte_perm(e.y, 0, y >= __uint_as_float(e.x) ? 0x4441 : 0x4440);
+    return decode_field(f, is_int4(h.qmin, h.qmax));
 }
 
 __device__ __forceinline__ float next_down(float y) {   // largest float < y (y finite, != -0)
@@ -135,14 +152,15 @@ __global__ void finalize_kernel(Header* h, uint2* cells, Change* chg) {
         int cnt = 0;
         float thr = 0.0f;
         int below = run, above = run;
-        while (p < n && cell_of(chg[p].y, h->c0, h->inv_w, h->ncell) == i) {
+        while (p < n && (int)cell_u(chg[p].y, h->c0, h->inv_w, (uint32_t)h->ncell) == i) {
             if (cnt == 0) { thr = chg[p].y; if (chg[p].before != run) ok = false; }
             run = chg[p].after;
             above = run;
             ++cnt;
             ++p;
         }
-        uint32_t meta = (uint32_t)(below & 0xFF) | ((uint32_t)(above & 0xFF) << 8) | (cnt > 1 ? 0x10000u : 0u);
+        const uint32_t fm = is_int4(h->qmin, h->qmax) ? 0xFu : 0xFFu;
+        uint32_t meta = (uint32_t)(below & fm) | ((uint32_t)(above & fm) << 8) | (cnt > 1 ? 0x10000u : 0u);
         const float t = cnt == 0 ? __int_as_float(0x7f800000) : thr;   // +inf: never reached
         cells[i] = make_uint2(__float_as_uint(t), meta);
     }
