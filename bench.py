@@ -322,6 +322,10 @@ def run_ours(args):
     if rank == 0 and not args.no_compare:
         cmp = compare_float_layers(torch, p, dev, ms, args)
 
+    t2 = None
+    if rank == 0 and not args.no_table2:
+        t2 = table2(torch, dev)
+
     result = None
     if rank == 0:
         cpu = None if (args.no_cpu or world > 1) else cpu_baseline(sample_seqs=1)
@@ -354,6 +358,7 @@ def run_ours(args):
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
             "paper_comparison": cmp,
+            "table2_bert_base_varlen": t2,
         }
         print(json.dumps(result))
     if world > 1:
@@ -404,6 +409,96 @@ def compare_float_layers(torch, p, dev, int4_ms, args):
     out["paper_context"] = "MKQ-BERT Table 2 (P:250-264): int4 15x vs fp32 for one BERT-base layer, NVIDIA T4, BS64"
     torch.backends.cuda.matmul.allow_tf32 = True
     return out
+
+
+# ------------------------------------------------------------------ paper Table 2 workload
+TABLE2 = [(16, 440), (16, 537), (16, 681), (64, 1691), (64, 2011), (64, 2298)]   # P:258-264 (BS, valid tokens)
+TABLE2_T4_US = {(16, 440): (1380, 213.1, 160.5), (16, 537): (1845, 245.7, 179.3), (16, 681): (2690, 260.9, 196.5),
+                (64, 1691): (6398, 567.4, 428.8), (64, 2011): (7185, 628.4, 490.1), (64, 2298): (7897, 669.9, 533.4)}
+
+
+def table2(torch, dev, reps=50):
+    """Paper Table 2 methodology on B200: one BERT-base layer
+    (h 768, 12 heads, FFN 3072) over BS sequences of max length 128 with the
+    given number of valid (non-padding) tokens, packed (cu_seqlens, R13);
+    int4 (W4A4) and int8 (W8A8) layers through mkq_bert_layer captured in a
+    CUDA graph, fp32 (TF32 off) torch/cuBLAS layer on the padded batch;
+    mean of `reps` CUDA-graph replays / eager runs."""
+    import synth
+    import torch.nn.functional as Fn
+    from paper_2203_13483_b200 import mkq as M
+    from paper_2203_13483_b200 import model
+    h, H, F, S = 768, 12, 3072, 128
+    p = synth.layer_params(h, H, F, 0)
+    layers = {}
+    for bits in (4, 8):
+        L = model.build_layer(p, bits, dev)
+        hc = torch.from_numpy(synth.hidden_states(8, S, h, seed=1000000)).to(dev)
+        model.calibrate(L, hc, 8, S)
+        layers[bits] = L
+    W = {k: torch.from_numpy(getattr(p, k)).to(dev) for k in
+         ("w_qkv", "b_qkv", "w_o", "b_o", "w_1", "b_1", "w_2", "b_2", "ln1_g", "ln1_b", "ln2_g", "ln2_b")}
+    torch.backends.cuda.matmul.allow_tf32 = False
+    rows = []
+    for bs, valid in TABLE2:
+        lens = synth.varlen_seqlens(bs, valid, S, seed=bs + valid)
+        cu = torch.tensor(np.concatenate([[0], np.cumsum(lens)]).astype(np.int32), device=dev)
+        hin = torch.from_numpy(synth.hidden_states(1, valid, h, seed=1)).to(dev)
+        res = {"bs": bs, "valid_tokens": valid}
+        for bits in (4, 8):
+            L = layers[bits]
+            out = torch.empty_like(hin)
+            ws = torch.empty(L.workspace_size(valid), dtype=torch.uint8, device=dev)
+            st = torch.cuda.Stream(device=dev)
+            with torch.cuda.stream(st):
+                for _ in range(3):
+                    M.mkq_bert_layer(L, hin, bs, S, cu, h_out=out, ws=ws, stream=st)
+            torch.cuda.synchronize(dev)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=st):
+                M.mkq_bert_layer(L, hin, bs, S, cu, h_out=out, ws=ws, stream=st)
+            g.replay()
+            torch.cuda.synchronize(dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(reps):
+                g.replay()
+            e1.record()
+            torch.cuda.synchronize(dev)
+            res[f"int{bits}_us"] = round(e0.elapsed_time(e1) / reps * 1e3, 1)
+        # fp32 torch layer on the padded batch (key padding mask)
+        x = torch.zeros(bs, S, h, device=dev)
+        mask = torch.zeros(bs, S, dtype=torch.bool, device=dev)
+        for i, Lq in enumerate(lens):
+            mask[i, :Lq] = True
+        am = torch.where(mask[:, None, None, :], 0.0, float("-inf"))
+
+        def layer32(xx):
+            qkv = Fn.linear(xx, W["w_qkv"], W["b_qkv"]).view(bs, S, 3, H, 64)
+            q, k, v = qkv.unbind(2)
+            a = Fn.scaled_dot_product_attention(q.transpose(1, 2), k.transpose(1, 2), v.transpose(1, 2), attn_mask=am)
+            a = a.transpose(1, 2).reshape(bs, S, h)
+            h1 = Fn.layer_norm(Fn.linear(a, W["w_o"], W["b_o"]) + xx, (h,), W["ln1_g"], W["ln1_b"], 1e-12)
+            f = Fn.linear(Fn.gelu(Fn.linear(h1, W["w_1"], W["b_1"])), W["w_2"], W["b_2"])
+            return Fn.layer_norm(f + h1, (h,), W["ln2_g"], W["ln2_b"], 1e-12)
+
+        for _ in range(3):
+            layer32(x)
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            layer32(x)
+        e1.record()
+        torch.cuda.synchronize(dev)
+        res["fp32_us"] = round(e0.elapsed_time(e1) / reps * 1e3, 1)
+        res["int4_vs_fp32"] = round(res["fp32_us"] / res["int4_us"], 2)
+        res["int4_vs_int8"] = round(res["int8_us"] / res["int4_us"], 2)
+        t4 = TABLE2_T4_US[(bs, valid)]
+        res["paper_T4_us_fp32_int8_int4"] = list(t4)
+        rows.append(res)
+    torch.backends.cuda.matmul.allow_tf32 = True
+    return rows
 
 
 # ------------------------------------------------------------------ oracle (CPU) arm
@@ -467,6 +562,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-compare", action="store_true", help="skip the fp32/bf16 torch comparison layer")
     ap.add_argument("--no-cpu", action="store_true", help="skip the oracle cpu_baseline")
+    ap.add_argument("--no-table2", action="store_true", help="skip the paper Table 2 (BERT-base varlen) rows")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

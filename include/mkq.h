@@ -190,6 +190,13 @@ MKQ_API mkq_status mkq_residual_layernorm(const float *x, const float *res, int6
                                   float *y, int bits, float s_q, int qmin, int qmax, void *q,
                                   int64_t ldq_bytes, void *stream);
 
+/* Column-parallel FFN plumbing: an NCCL all_gather of per-rank
+ * column blocks yields src = [g][rows][cb] bytes (rank-major); this writes
+ * dst[row][r*cb + j] = src[r][row][j] with row stride ld_dst bytes.
+ * src/dst [device], 16-byte aligned, cb % 16 == 0, ld_dst >= g*cb. */
+MKQ_API mkq_status mkq_interleave_blocks(const void *src, void *dst, int64_t g, int64_t rows, int64_t cb,
+                                         int64_t ld_dst_bytes, void *stream);
+
 /* ------------------------------------------------------------------------
  * One quantized post-LN BERT encoder layer (§8a rows a1-a8 composed):
  *   c   = Q(h; s_qkv_in)                                   a1

@@ -587,6 +587,23 @@ mkq_status mkq_residual_layernorm(const float* x, const float* res, int64_t rows
     return e == cudaSuccess ? MKQ_OK : cuda_fail(e, "layernorm launch");
 }
 
+mkq_status mkq_interleave_blocks(const void* src, void* dst, int64_t g, int64_t rows, int64_t cb, int64_t ldd,
+                                 void* stream) {
+    if (g < 0 || rows < 0 || cb < 0) return fail(MKQ_ERR_SHAPE, "negative dimension");
+    if (g == 0 || rows == 0 || cb == 0) return MKQ_OK;
+    if (!src || !dst) return fail(MKQ_ERR_NULL, "src and dst are required");
+    if (cb % 16 || ldd < g * cb || ldd % 16) return fail(MKQ_ERR_SHAPE, "cb % 16, ld_dst >= g*cb, ld_dst % 16");
+    if (!aligned16(src) || !aligned16(dst)) return fail(MKQ_ERR_ALIGN, "src/dst must be 16-byte aligned");
+    int sms = 0;
+    mkq_status s = check_device(&sms);
+    if (s != MKQ_OK) return s;
+    const int gr = grid_for(g * rows * (cb / 16), 256, sms);
+    mkq::interleave_blocks_kernel<<<gr, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const uint8_t*>(src), static_cast<uint8_t*>(dst), g, rows, cb, ldd);
+    cudaError_t e = cudaPeekAtLastError();
+    return e == cudaSuccess ? MKQ_OK : cuda_fail(e, "interleave launch");
+}
+
 // ------------------------------------------------------------------ BERT layer
 struct LayerWs {
     size_t codes_in, qkv, codes_oa, o, h1, codes_h1, codes_ffn2, f, total;

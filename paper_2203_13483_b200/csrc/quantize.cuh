@@ -107,3 +107,19 @@ __global__ void absmax_finalize_kernel(const unsigned int* gmax_bits, float l_ma
 }
 
 }  // namespace mkq
+
+namespace mkq {
+// Rank-major all-gather result [g][rows][cb] -> row-major [rows][g*cb]
+// (column-parallel FFN: the FFN2 input codes / the FFN2 output columns).
+// One thread per 16-byte chunk; cb % 16 == 0.
+__global__ void __launch_bounds__(256) interleave_blocks_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
+                                                                int64_t g, int64_t rows, int64_t cb, int64_t ldd) {
+    const int64_t cpr = cb / 16;                  // chunks per (rank, row)
+    const int64_t total = g * rows * cpr;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = i % cpr, rr = (i / cpr) % rows, r = i / (cpr * rows);
+        const uint4 v = __ldcs(reinterpret_cast<const uint4*>(src + (r * rows + rr) * cb) + c);
+        *(reinterpret_cast<uint4*>(dst + rr * ldd + r * cb) + c) = v;
+    }
+}
+}  // namespace mkq

@@ -14,7 +14,7 @@ from ._lib import (OUT_BF16, OUT_F16, OUT_F32, OUT_I32, OUT_I4, OUT_I8, MkqEpilo
                    check, lib)
 
 __all__ = ["mkq_requant_table", "mkq_quantize_pack", "mkq_absmax_scale", "mkq_gemm_w4a4", "mkq_gemm_w8a8",
-           "mkq_attention", "mkq_residual_layernorm", "mkq_bert_layer", "out_dtype_bytes",
+           "mkq_attention", "mkq_residual_layernorm", "mkq_bert_layer", "mkq_interleave_blocks", "out_dtype_bytes",
            "OUT_F32", "OUT_BF16", "OUT_I32", "OUT_I4", "OUT_I8", "OUT_F16"]
 
 
@@ -160,6 +160,16 @@ def mkq_residual_layernorm(x: torch.Tensor, res: Optional[torch.Tensor], g: torc
         _ptr(x), _ptr(res), rows, cols, x.stride(0), _ptr(g), _ptr(b), float(eps), _ptr(y), bits, float(s_q), qmin,
         qmax, _ptr(q), _row_bytes(q) if q is not None else 0, _stream(stream)))
     return (y, q) if bits else y
+
+
+def mkq_interleave_blocks(src: torch.Tensor, g: int, rows: int, cb: int, out: Optional[torch.Tensor] = None,
+                          stream=None) -> torch.Tensor:
+    """[g][rows][cb] bytes (rank-major all-gather) -> [rows][g*cb] bytes."""
+    if out is None:
+        out = torch.empty((rows, g * cb), dtype=torch.uint8, device=src.device)
+    check("mkq_interleave_blocks", lib().mkq_interleave_blocks(_ptr(src), _ptr(out), g, rows, cb,
+                                                               out.stride(0) * out.element_size(), _stream(stream)))
+    return out
 
 
 class QLayer:
