@@ -36,7 +36,7 @@ struct Epi2Params {
     const void* table;   // rq table (global) or null
 };
 
-template <int BN_>
+template <int BN_, int EPI_ = 8, int UNP_ = 8>
 struct Gemm2Cfg {
     static constexpr int BM = 128;                  // A rows per CTA (MMA M = 256 per pair)
     static constexpr int BN = BN_;                  // MMA N (per pair)
@@ -50,12 +50,15 @@ struct Gemm2Cfg {
     static constexpr int kStageP = kAP + kBP;
     static constexpr int S8 = 4;
     static constexpr int SP = 3;
-    static constexpr int kEpiWarps = 8;
-    static constexpr int kUnpWarps = 8;
+    static constexpr int kEpiWarps = EPI_;          // 8 or 16 (2 or 4 per TMEM lane quadrant)
+    static constexpr int kUnpWarps = UNP_;          // 8 or 4
     static constexpr int kThreads = 32 * (4 + kEpiWarps + kUnpWarps);
     static constexpr uint32_t kTmemCols = 2 * BN;
     static constexpr int kScb = 2 * BN * 8;          // 2 buffers x BN x (sc, b)
-    static constexpr int kStaging = kEpiWarps * 4096; // 32 rows x 128 B output block per warp
+    static constexpr int kStagePerWarp = 2048;      // 32 rows x 64 B output block per warp
+    static constexpr int kStaging = kEpiWarps * kStagePerWarp;
+    static constexpr int kColsPerWarp = BN / (kEpiWarps / 4);
+    static_assert(kColsPerWarp % 32 == 0, "epilogue column split");
     static constexpr int kBarBytes = 8 * (2 * S8 + 2 * SP + 4) + 16;
     static constexpr int kSmem = 1024 + S8 * kStage8 + SP * kStageP + (int)rq::kSmemBytes + kScb + kStaging + kBarBytes;
     static_assert(kSmem <= 232448, "shared memory budget");
@@ -115,8 +118,10 @@ __device__ __forceinline__ uint32_t stg_off(int r, int c, int P) {
     return (uint32_t)(r * P + ((c ^ f) << 4));
 }
 
-__device__ __forceinline__ int out_pitch(int mode) {   // bytes per row of a 32-column block
-    return mode == OUT_F32 || mode == OUT_I32 ? 128 : (mode == OUT_I4 ? 16 : (mode == OUT_I8 ? 32 : 64));
+// bytes per staged row: 4-byte outputs are staged and stored 16 columns at a
+// time (64 B), 2-byte outputs 32 columns (64 B), int8 32 (32 B), int4 32 (16 B)
+__device__ __forceinline__ int out_pitch(int mode) {
+    return mode == OUT_F32 || mode == OUT_I32 ? 64 : (mode == OUT_I4 ? 16 : (mode == OUT_I8 ? 32 : 64));
 }
 
 // 16 outputs (columns cl..cl+15 of one accumulator row) -> staging row `r`,
@@ -131,7 +136,7 @@ __device__ __forceinline__ void epi2_half(const EpiParams& ep, const Lut& L, boo
     if (mode == OUT_I32) {
 #pragma unroll
         for (int c = 0; c < 4; ++c)
-            *reinterpret_cast<int4*>(stage + stg_off(r, h2 * 4 + c, P)) =
+            *reinterpret_cast<int4*>(stage + stg_off(r, c, P)) =
                 make_int4(acc[4 * c], acc[4 * c + 1], acc[4 * c + 2], acc[4 * c + 3]);
         return;
     }
@@ -181,7 +186,7 @@ __device__ __forceinline__ void epi2_half(const EpiParams& ep, const Lut& L, boo
     if (mode == OUT_F32) {
 #pragma unroll
         for (int c = 0; c < 4; ++c)
-            *reinterpret_cast<float4*>(stage + stg_off(r, h2 * 4 + c, P)) =
+            *reinterpret_cast<float4*>(stage + stg_off(r, c, P)) =
                 make_float4(y[4 * c], y[4 * c + 1], y[4 * c + 2], y[4 * c + 3]);
     } else {
         uint32_t w[8];
@@ -305,7 +310,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
         // ---------------------------------------------------- epilogue (both CTAs)
         const int e = warp - 4;           // 0..7
         const int q = warp & 3;           // TMEM lane quadrant (warp % 4)
-        const int h = e >> 2;             // column half
+        const int h = e >> 2;             // column part (kColsPerWarp columns)
         const int et = threadIdx.x - 128; // 0..255
         bool use_table = false;
         if (p.table) {
@@ -319,7 +324,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
                         th->qmax == ep.qmax;
         Lut L{0.0f, 0.0f, 1, ptx::smem_u32(tcells)};
         if (use_table) L = Lut{th->c0, th->inv_w, th->ncell, ptx::smem_u32(tcells)};
-        uint8_t* stage = staging + e * 4096;
+        uint8_t* stage = staging + e * Cfg::kStagePerWarp;
         if (lane == 0) ptx::tma_prefetch_desc(&tmO);
         int it = 0;
         for (int tile = cluster; tile < num_tiles; tile += nclusters, ++it) {
@@ -338,25 +343,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
             ptx::tc_fence_after();
             const int row0 = m0 + q * 32;
 #pragma unroll 1
-            for (int j = 0; j < BN / 2 / 32; ++j) {
-                const int cl = h * (BN / 2) + 32 * j;
+            for (int j = 0; j < Cfg::kColsPerWarp / 32; ++j) {
+                const int cl = h * Cfg::kColsPerWarp + 32 * j;
                 const int n = n0 + cl;
                 if (n >= N) break;
-                // the previous TMA store must have finished reading the staging block
-                if (lane == 0) ptx::tma_store_wait_read<0>();
-                __syncwarp();
+                const bool wide = ep.mode == OUT_F32 || ep.mode == OUT_I32;   // two 16-column stores
 #pragma unroll
                 for (int h2 = 0; h2 < 2; ++h2) {
+                    if (h2 == 0 || wide) {
+                        // the previous TMA store must have finished reading the staging block
+                        if (lane == 0) ptx::tma_store_wait_read<0>();
+                        __syncwarp();
+                    }
                     uint32_t v[16];
                     ptx::tmem_ld_32x32b_x16(tmem_base + ((uint32_t)(q * 32) << 16) + ab * BN + cl + 16 * h2, v);
                     ptx::tmem_ld_wait();
                     epi2_half(ep, L, use_table, ptx::smem_u32(sb + cl + 16 * h2), v, stage, lane, h2);
-                }
-                ptx::fence_proxy_async_smem();
-                __syncwarp();
-                if (lane == 0) {
-                    ptx::tma_store_2d(&tmO, stage, ep.mode == OUT_I4 ? n / 2 : n, row0);
-                    ptx::tma_store_commit();
+                    if (h2 == 1 || wide) {
+                        ptx::fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {
+                            const int nn = n + (wide ? 16 * h2 : 0);
+                            ptx::tma_store_2d(&tmO, stage, ep.mode == OUT_I4 ? nn / 2 : nn, row0);
+                            ptx::tma_store_commit();
+                        }
+                    }
                 }
             }
             ptx::tc_fence_before();
@@ -369,8 +380,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
         const int u = threadIdx.x - 32 * (4 + Cfg::kEpiWarps);
         constexpr int kChunks = (BM + BNH) * (Cfg::BK / 32);   // 16-byte packed chunks per stage
         constexpr int kPer = kChunks / kUnpThreads;
-        static_assert(kChunks % kUnpThreads == 0 && kUnpThreads == 256, "chunk split: 64 rows per pass");
-        // Thread u always handles 16-byte chunk c = u & 3 of rows r = (u >> 2) + 64 i:
+        static_assert(kChunks % kUnpThreads == 0, "chunk split");
+        constexpr uint32_t kRowsPerPass = kUnpThreads / 4;
+        // Thread u always handles 16-byte chunk c = u & 3 of rows r = (u >> 2) + (threads/4) i:
         // its swizzle phase (r & 7) and both destination offsets are loop invariants.
         const uint32_t r0 = (uint32_t)u >> 2, c = (uint32_t)u & 3u, r7 = r0 & 7u;
         const uint32_t src_off = r0 * 64u + c * 16u;
@@ -386,7 +398,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
                 uint4 pk[kPer];
 #ifndef MKQ_DBG_NO_UNPACK
 #pragma unroll
-                for (int i = 0; i < kPer; ++i) pk[i] = ptx::lds128(src + (uint32_t)i * (64u * 64u));
+                for (int i = 0; i < kPer; ++i) pk[i] = ptx::lds128(src + (uint32_t)i * (kRowsPerPass * 64u));
 #endif
                 ptx::mbar_wait(&empty8[s8], ph8 ^ 1);
                 const uint32_t dst = ring8_s + (uint32_t)s8 * Cfg::kStage8;
@@ -399,7 +411,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
                     lo.y = (pv.y * 16u) & 0xF0F0F0F0u; hi.y = pv.y & 0xF0F0F0F0u;
                     lo.z = (pv.z * 16u) & 0xF0F0F0F0u; hi.z = pv.z & 0xF0F0F0F0u;
                     lo.w = (pv.w * 16u) & 0xF0F0F0F0u; hi.w = pv.w & 0xF0F0F0F0u;
-                    const uint32_t rb = dst + (uint32_t)i * (64u * 128u);
+                    const uint32_t rb = dst + (uint32_t)i * (kRowsPerPass * 128u);
                     ptx::sts128(rb + dlo_off, lo);
                     ptx::sts128(rb + dhi_off, hi);
                 }

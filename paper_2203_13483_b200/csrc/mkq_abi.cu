@@ -132,14 +132,15 @@ mkq_status make_map(CUtensorMap* out, const void* base, uint64_t inner, uint64_t
                       swz128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE);
 }
 
-// Output map of the 2-CTA epilogue: 32-column x 32-row blocks staged in
-// shared memory with the swizzle matching mkq::stg_off().
+// Output map of the 2-CTA epilogue: 32-row blocks (16 columns of 4-byte
+// outputs, 32 columns otherwise) staged in shared memory with the swizzle
+// matching mkq::stg_off().
 mkq_status make_out_map(CUtensorMap* out, void* base, int mode, int64_t M, int64_t N, int64_t ldo) {
     switch (mode) {
     case MKQ_OUT_F32:
-        return make_map_t(out, base, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, N, M, ldo, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+        return make_map_t(out, base, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, N, M, ldo, 16, 32, CU_TENSOR_MAP_SWIZZLE_64B);
     case MKQ_OUT_I32:
-        return make_map_t(out, base, CU_TENSOR_MAP_DATA_TYPE_INT32, N, M, ldo, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+        return make_map_t(out, base, CU_TENSOR_MAP_DATA_TYPE_INT32, N, M, ldo, 16, 32, CU_TENSOR_MAP_SWIZZLE_64B);
     case MKQ_OUT_F16:
         return make_map_t(out, base, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, N, M, ldo, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
     case MKQ_OUT_BF16:
@@ -273,8 +274,15 @@ mkq_status gemm_common(bool int4, const void* a, int64_t lda, const void* w, int
     if (int4 && two_cta) {
         mkq::Epi2Params p2{ep, (e.out == MKQ_OUT_I4 || e.out == MKQ_OUT_I8) ? e.requant_table : nullptr};
         if (p2.table && !aligned16(p2.table)) return fail(MKQ_ERR_ALIGN, "requant_table must be 16-byte aligned");
-        if (N % 256 == 0)
+        // K <= 1024 tiles are epilogue-bound (8 K-blocks per tile): 16 epilogue + 4
+        // unpack warps; longer K keeps 8 + 8 (mainloop-bound)
+        static const int epi_override = [] { const char* v = getenv("MKQ_EPI_WARPS"); return v ? atoi(v) : 0; }();
+        const bool many_epi = epi_override ? epi_override == 16 : K <= 1024;
+        if (N % 256 == 0) {
+            if (many_epi)
+                return launch_gemm2<mkq::Gemm2Cfg<256, 16, 4>>(a, lda, w, ldw, (int)M, (int)N, (int)K, p2, sms, st);
             return launch_gemm2<mkq::Gemm2Cfg<256>>(a, lda, w, ldw, (int)M, (int)N, (int)K, p2, sms, st);
+        }
         return launch_gemm2<mkq::Gemm2Cfg<128>>(a, lda, w, ldw, (int)M, (int)N, (int)K, p2, sms, st);
     }
     if (int4) {
