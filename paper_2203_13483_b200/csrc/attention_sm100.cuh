@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     uint64_t* kv_empty = v_full + kStages;          // [kStages]
     uint64_t* s_full = kv_empty + kStages;          // [2]
     uint64_t* p_ready = s_full + 2;                 // [2]
-    uint64_t* pv_done = p_ready + 2;                // [2] (per O buffer)
+    uint64_t* pv_done = p_ready + 2;                // [2] (by block parity)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -222,6 +222,10 @@ __global__ void __launch_bounds__(kThreads, 2)
                 }
                 ++it;
             }
+            // tail: every ring slot and Q buffer released, i.e. every tcgen05.commit
+            // arrive on this CTA's barriers has landed before the CTA can exit
+            for (int i = 0; i < kStages; ++i, ++g) ptx::mbar_wait(&kv_empty[g % kStages], ((g / kStages) & 1) ^ 1);
+            for (int i = 0; i < 2; ++i, ++it) ptx::mbar_wait(&q_empty[it & 1], ((it >> 1) & 1) ^ 1);
         }
     } else if (warp == 1) {
         // ---------------------------------------------------- MMA issuer
@@ -272,7 +276,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                     mma_f16_ts(tO, tS[cur.g & 1] + 8 * k, desc_sw128_mnmajor(v_addr + 2048 * k), idO,
                                (cur.j | k) != 0);
                 ptx::mma_commit(&kv_empty[st]);
-                ptx::mma_commit(&pv_done[0]);
+                ptx::mma_commit(&pv_done[cur.g & 1]);
                 if (cur.j + 1 == cur.nblk) ptx::mma_commit(&q_empty[cur.it & 1]);
                 cur = nxt;
             }
@@ -325,7 +329,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                     const float alpha = ex2f(m - m_new);   // 0 when m = -inf, 1 when !up
                     l *= alpha;
                     if (j > 0) {   // O holds PV_0..PV_{j-1}: wait for PV_{j-1}, then scale our 32 dims
-                        ptx::mbar_wait(&pv_done[0], (g - 1) & 1);
+                        ptx::mbar_wait(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
                         ptx::tc_fence_after();
                         uint32_t o[32];
                         ptx::tmem_ld_32x32b_x32(tO + lane_off + 32 * hf, o);
@@ -353,9 +357,12 @@ __global__ void __launch_bounds__(kThreads, 2)
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(&p_ready[g & 1]);
+                // consume PV_{j-1}'s completion (cheap: it was issued a block ago); keeps
+                // every phase of the two pv_done barriers waited on
+                if (j > 0) ptx::mbar_wait(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
             }
             // O after the last PV of this item
-            ptx::mbar_wait(&pv_done[0], (g - 1) & 1);
+            ptx::mbar_wait(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
             ptx::tc_fence_after();
             float R[kD / 2];
             {

@@ -257,6 +257,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
     if (warp == 2) ptx::tmem_alloc_2cta<Cfg::kTmemCols>(tmem_slot);
     ptx::tc_fence_before();
     ptx::cluster_sync();
+    __syncthreads();   // CTA barrier as well (orders the slot write for tools that do not model barrier.cluster)
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
@@ -429,6 +430,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
                 if (++sp == SP) { sp = 0; php ^= 1; }
                 if (++s8 == S8) { s8 = 0; ph8 ^= 1; }
             }
+        }
+        // tail: wait until the MMA's last multicast commits on empty8 have landed
+        for (int i = 0; i < S8; ++i) {
+            ptx::mbar_wait(&empty8[s8], ph8 ^ 1);
+            if (++s8 == S8) { s8 = 0; ph8 ^= 1; }
         }
     }
 

@@ -225,6 +225,12 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
                     }
                 }
             }
+            if constexpr (!kInt4) {   // tail: the MMA's last commits on empty8 have landed
+                for (int i = 0; i < S8; ++i) {
+                    ptx::mbar_wait(&empty8[s], ph ^ 1);
+                    if (++s == S8) { s = 0; ph ^= 1; }
+                }
+            }
         }
     } else if (warp == 1) {
         // ---------------------------------------------------- MMA issuer
@@ -312,6 +318,10 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
                 if (++sp == SP) { sp = 0; php ^= 1; }
                 if (++s8 == S8) { s8 = 0; ph8 ^= 1; }
             }
+        }
+        for (int i = 0; i < S8; ++i) {   // tail: the MMA's last commits on empty8 have landed
+            ptx::mbar_wait(&empty8[s8], ph8 ^ 1);
+            if (++s8 == S8) { s8 = 0; ph8 ^= 1; }
         }
     }
 
