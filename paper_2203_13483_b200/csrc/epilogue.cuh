@@ -22,6 +22,76 @@ __device__ __forceinline__ int quant_code(float x, float s, int qmin, int qmax) 
     return min(max(q, qmin), qmax);
 }
 
+// Eq.1 without a division per element, for epilogues that quantize many
+// values by one scale: q = x*r corrected once by the remainder
+// (r = RN(1/s); rem = x - q*s is exact in the fma; q' = q + rem*r), clamped
+// to [qmin, qmax] (clamp and rint commute for integer bounds) and rounded
+// with the 1.5*2^23 magic add (exact for |q| <= 2^22).  q' is within an ulp
+// or two of x/s, so its code can differ from quant_code's only when q' lies
+// within a few ulps of a half-integer rounding boundary: `near` reports that
+// case and the caller recomputes those values with quant_code (rare).
+struct QuantRcp {
+    float s, r, lo, hi;
+    int qmin, qmax;
+};
+__device__ __forceinline__ QuantRcp quant_rcp(float s, int qmin, int qmax) {
+    return QuantRcp{s, __frcp_rn(s), (float)qmin, (float)qmax, qmin, qmax};
+}
+__device__ __forceinline__ int quant_code_rcp(float x, const QuantRcp& Q, bool& near) {
+    float q = __fmul_rn(x, Q.r);
+    const float rem = __fmaf_rn(-q, Q.s, x);
+    q = __fmaf_rn(rem, Q.r, q);
+    q = fminf(fmaxf(q, Q.lo), Q.hi);   // NaN -> lo, like quant_code
+    const float t = __fadd_rn(q, 12582912.0f);
+    const float d = __fsub_rn(q, __fsub_rn(t, 12582912.0f));   // q - rint(q), in [-0.5, 0.5]
+    near |= fabsf(__fsub_rn(fabsf(d), 0.5f)) <= __fmul_rn(fabsf(q), 0x1p-20f);
+    return __float_as_int(t) - 0x4B400000;
+}
+
+// A group of codes with one near-boundary check (the exact fallback is taken
+// for the whole group, keeping the common path branch-free).
+template <int N>
+__device__ __forceinline__ void quant_group_rcp(const float (&v)[N], const QuantRcp& Q, int (&c)[N]) {
+    bool near = false;
+#pragma unroll
+    for (int i = 0; i < N; ++i) c[i] = quant_code_rcp(v[i], Q, near);
+    if (near) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) c[i] = quant_code(v[i], Q.s, Q.qmin, Q.qmax);
+    }
+}
+
+// Out-of-line exact fallbacks for code-size-sensitive epilogues (the
+// near-boundary case is rare; keeping the IEEE divisions out of line keeps
+// the hot loop in the instruction cache).
+__device__ __noinline__ uint32_t quant_nib8_exact(float v0, float v1, float v2, float v3, float v4, float v5, float v6,
+                                                  float v7, float s, int qmin, int qmax) {
+    const float v[8] = {v0, v1, v2, v3, v4, v5, v6, v7};
+    uint32_t w = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) w |= (uint32_t)(quant_code(v[i], s, qmin, qmax) & 0xF) << (4 * i);
+    return w;
+}
+__device__ __noinline__ uint32_t quant_byte4_exact(float v0, float v1, float v2, float v3, float s, int qmin, int qmax) {
+    return (uint32_t)(quant_code(v0, s, qmin, qmax) & 0xFF) | ((uint32_t)(quant_code(v1, s, qmin, qmax) & 0xFF) << 8) |
+           ((uint32_t)(quant_code(v2, s, qmin, qmax) & 0xFF) << 16) | ((uint32_t)(quant_code(v3, s, qmin, qmax) & 0xFF) << 24);
+}
+__device__ __forceinline__ uint32_t quant_nib8_rcp(const float (&v)[8], const QuantRcp& Q) {
+    bool near = false;
+    uint32_t w = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) w |= (uint32_t)(quant_code_rcp(v[i], Q, near) & 0xF) << (4 * i);
+    if (near) w = quant_nib8_exact(v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7], Q.s, Q.qmin, Q.qmax);
+    return w;
+}
+__device__ __forceinline__ uint32_t quant_byte4_rcp(float v0, float v1, float v2, float v3, const QuantRcp& Q) {
+    bool near = false;
+    const int c0 = quant_code_rcp(v0, Q, near), c1 = quant_code_rcp(v1, Q, near);
+    const int c2 = quant_code_rcp(v2, Q, near), c3 = quant_code_rcp(v3, Q, near);
+    if (near) return quant_byte4_exact(v0, v1, v2, v3, Q.s, Q.qmin, Q.qmax);
+    return (uint32_t)(c0 & 0xFF) | ((uint32_t)(c1 & 0xFF) << 8) | ((uint32_t)(c2 & 0xFF) << 16) | ((uint32_t)(c3 & 0xFF) << 24);
+}
+
 // Dequant (P:66 s*q, P:93/P:98 bias; reading R4).
 __device__ __forceinline__ float dequant(int32_t acc, float sc, float b, bool has_bias) {
     float a = __int2float_rn(acc);

@@ -281,8 +281,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
         }
     } else if (warp == 1) {
         // ---------------------------------------------------- MMA issuer (leader CTA)
-        if (rank == 0 && lane == 0) {
+        // Whole warp converged; elect.sync inside the MMA/commit wrappers picks
+        // the issuing lane (3x cheaper per MMA than a diverged single lane).
+        if (rank == 0) {
             constexpr uint32_t idesc = ptx::idesc_i8(2 * BM, BN);
+            const uint64_t dA0 = ptx::desc_sw128_kmajor(ptx::smem_u32(ring8));
             int s = 0;
             uint32_t ph = 0;
             int it = 0;
@@ -295,16 +298,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
                 for (int kb = 0; kb < nk; ++kb) {
                     ptx::mbar_wait(&full8[s], ph);
                     ptx::tc_fence_after();
-                    const uint32_t a_addr = ptx::smem_u32(ring8 + s * Cfg::kStage8);
-                    const uint32_t b_addr = a_addr + Cfg::kA8;
+                    const uint64_t da = dA0 + (uint64_t)((s * Cfg::kStage8) >> 4);
+                    const uint64_t db = da + (uint64_t)(Cfg::kA8 >> 4);
 #pragma unroll
                     for (int k = 0; k < Cfg::BK / 32; ++k)
-                        ptx::mma_i8_ss_2cta(d, ptx::desc_sw128_kmajor(a_addr + 32 * k),
-                                            ptx::desc_sw128_kmajor(b_addr + 32 * k), idesc, (kb | k) != 0);
-                    ptx::mma_commit_2cta_mc(&empty8[s], 3);
+                        ptx::mma_i8_ss_2cta_warp(d, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+                    ptx::mma_commit_2cta_mc_warp(&empty8[s], 3);
                     if (++s == S8) { s = 0; ph ^= 1; }
                 }
-                ptx::mma_commit_2cta_mc(&tfull[ab], 3);
+                ptx::mma_commit_2cta_mc_warp(&tfull[ab], 3);
             }
         }
     } else if (warp >= 4 && warp < 4 + Cfg::kEpiWarps) {

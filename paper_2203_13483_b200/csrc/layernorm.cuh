@@ -26,6 +26,7 @@ __global__ void __launch_bounds__(256) residual_ln_kernel(
     const int lane = threadIdx.x & 31;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
     const int nv = cols >> 2;
+    const QuantRcp Qr = quant_rcp(s_q, qmin, qmax);
     for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += warps) {
         const float4* xr = reinterpret_cast<const float4*>(x + r * ld);
         const float4* rr = res ? reinterpret_cast<const float4*>(res + r * ld) : nullptr;
@@ -70,15 +71,17 @@ __global__ void __launch_bounds__(256) residual_ln_kernel(
                 o.z = (v[i].z - mean) * rstd * gg.z + bb.z;
                 o.w = (v[i].w - mean) * rstd * gg.w + bb.w;
                 yr[c] = o;
-                if (bits == 4) {
-                    const int c0 = quant_code(o.x, s_q, qmin, qmax), c1 = quant_code(o.y, s_q, qmin, qmax);
-                    const int c2 = quant_code(o.z, s_q, qmin, qmax), c3 = quant_code(o.w, s_q, qmin, qmax);
-                    const uint16_t w = (uint16_t)((c0 & 0xF) | ((c1 & 0xF) << 4) | ((c2 & 0xF) << 8) | ((c3 & 0xF) << 12));
-                    *reinterpret_cast<uint16_t*>(q + r * ldq + 2 * c) = w;
-                } else if (bits == 8) {
-                    *reinterpret_cast<uint32_t*>(q + r * ldq + 4 * c) =
-                        pack_byte4(quant_code(o.x, s_q, qmin, qmax), quant_code(o.y, s_q, qmin, qmax),
-                                   quant_code(o.z, s_q, qmin, qmax), quant_code(o.w, s_q, qmin, qmax));
+                if (bits) {
+                    const float ov[4] = {o.x, o.y, o.z, o.w};
+                    int cq[4];
+                    quant_group_rcp(ov, Qr, cq);
+                    if (bits == 4) {
+                        const uint16_t w = (uint16_t)((cq[0] & 0xF) | ((cq[1] & 0xF) << 4) | ((cq[2] & 0xF) << 8) |
+                                                      ((cq[3] & 0xF) << 12));
+                        *reinterpret_cast<uint16_t*>(q + r * ldq + 2 * c) = w;
+                    } else {
+                        *reinterpret_cast<uint32_t*>(q + r * ldq + 4 * c) = pack_byte4(cq[0], cq[1], cq[2], cq[3]);
+                    }
                 }
             }
         }

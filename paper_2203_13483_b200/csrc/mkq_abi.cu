@@ -16,6 +16,7 @@
 #include "../../include/mkq.h"
 #include "attention.cuh"
 #include "attention_sm100.cuh"
+#include "attention_pp_sm100.cuh"
 #include "gemm_sm100.cuh"
 #include "gemm2_sm100.cuh"
 #include "requant.cuh"
@@ -502,12 +503,50 @@ mkq_status mkq_attention(const void* qkv, int64_t ld, int64_t batch, int64_t max
     }
     mkq_status s = check_device();
     if (s != MKQ_OK) return s;
-    static const int attn_path = [] {   // MKQ_ATTN=mma selects the mma.sync kernel (diagnostics)
+    static const int attn_path = [] {   // MKQ_ATTN=tc|mma select the older kernels (diagnostics)
         const char* v = getenv("MKQ_ATTN");
-        return (v && strcmp(v, "mma") == 0) ? 1 : 0;
+        if (v && strcmp(v, "mma") == 0) return 1;
+        if (v && strcmp(v, "tc") == 0) return 0;
+        return 2;
     }();
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (attn_path == 0) {
+    if (attn_path == 2) {
+        const int mi = out_mode == MKQ_OUT_F32 ? 0 : (out_mode == MKQ_OUT_I4 ? 1 : 2);
+        auto kern = mi == 0 ? mkq::attnpp::attn_pp_kernel<0>
+                            : (mi == 1 ? mkq::attnpp::attn_pp_kernel<3> : mkq::attnpp::attn_pp_kernel<4>);
+        static bool attr_set[3][64] = {};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (!attr_set[mi][dev]) {
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, mkq::attnpp::kSmem);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(attn_pp)");
+            attr_set[mi][dev] = true;
+        }
+        CUtensorMap mq, mkv;
+        s = make_map_t(&mq, qkv, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, (uint64_t)(3 * hidden), (uint64_t)tokens,
+                       (uint64_t)ld * 2, 64, mkq::attnpp::kBQ, CU_TENSOR_MAP_SWIZZLE_128B);
+        if (s != MKQ_OK) return s;
+        s = make_map_t(&mkv, qkv, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, (uint64_t)(3 * hidden), (uint64_t)tokens,
+                       (uint64_t)ld * 2, 64, mkq::attnpp::kBK, CU_TENSOR_MAP_SWIZZLE_128B);
+        if (s != MKQ_OK) return s;
+        mkq::attn2::Params p;
+        p.cu = cu;
+        p.seq = (int)max_seq;
+        p.hidden = (int)hidden;
+        p.out_mode = out_mode;
+        p.s_out = s_out;
+        p.qmin = qmin;
+        p.qmax = qmax;
+        p.out = out;
+        p.ldo = ldo;
+        int sms = 0;
+        check_device(&sms);
+        const int pairs = (int)((max_seq + 2 * mkq::attnpp::kBQ - 1) / (2 * mkq::attnpp::kBQ));
+        const int64_t nitems = (int64_t)batch * heads * pairs;
+        if (nitems > (1ll << 30)) return fail(MKQ_ERR_SHAPE, "too many attention work items");
+        const int grid = (int)(nitems < sms ? nitems : sms);   // persistent, 1 CTA per SM
+        kern<<<grid, mkq::attnpp::kThreads, mkq::attnpp::kSmem, st>>>(mq, mkv, p, heads, pairs, (int)nitems);
+    } else if (attn_path == 0) {
         static bool attr_set[64] = {};
         int dev = 0;
         cudaGetDevice(&dev);

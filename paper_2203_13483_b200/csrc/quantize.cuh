@@ -20,17 +20,17 @@ __global__ void __launch_bounds__(256) quantize_pack_vec_kernel(
     const int64_t per_row = cols >> 3;
     const int64_t total = rows * per_row;
     const float s_t = (kPerRow || !scale) ? s_val : __ldg(scale);
+    const QuantRcp Q_t = quant_rcp(s_t, qmin, qmax);
     for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total;
          g += (int64_t)gridDim.x * blockDim.x) {
         const int64_t r = g / per_row;
         const int64_t c8 = (g - r * per_row) << 3;
-        const float s = kPerRow ? __ldg(scale + r) : s_t;
+        const QuantRcp Q = kPerRow ? quant_rcp(__ldg(scale + r), qmin, qmax) : Q_t;
         const float4* src = reinterpret_cast<const float4*>(x + r * ldx + c8);
         const float4 a = __ldcs(src), b = __ldcs(src + 1);
         const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
         int c[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) c[i] = quant_code(v[i], s, qmin, qmax);
+        quant_group_rcp(v, Q, c);
         if constexpr (kBits == 4) {
             *reinterpret_cast<uint32_t*>(q + r * ldq + (c8 >> 1)) = pack_nib8(c);
         } else {

@@ -16,7 +16,7 @@ for _ in range(10):
     M.mkq_attention(qkv, H, B, S, None, mode=M.OUT_I4, s_out=0.05, out=out)
 e1.record(); torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / 10
-print(f"attention path={os.environ.get('MKQ_ATTN','tc')} B={B}: {ms*1e3:.1f} us, {4*T*S*hd/ms/1e9:.1f} TFLOP/s")
+print(f"attention path={os.environ.get('MKQ_ATTN','pp')} B={B}: {ms*1e3:.1f} us, {4*T*S*hd/ms/1e9:.1f} TFLOP/s")
 if os.environ.get("KNAMES"):
     from torch.profiler import profile, ProfilerActivity
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
