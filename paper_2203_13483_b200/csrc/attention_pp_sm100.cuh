@@ -302,10 +302,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // so one tile's exponentials overlap the other's MMAs instead
                 // of both tiles contending for the XU pipe in lock-step.
                 TRACE(3);
+#ifndef MKQ_ABL_NOSTAGGER
                 if (I.hasB) {
                     if (x == 0 && j > 0) ptx::named_bar_sync(5 + q, 64);
                     if (x == 1) ptx::named_bar_sync(1 + q, 64);
                 }
+#endif
                 TRACE(4);
                 const float nmx = -m;
                 float ps[4] = {0.0f, 0.0f, 0.0f, 0.0f};
@@ -313,6 +315,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ptx::mbar_wait(&pv_done[x], (nb - 1) & 1);
                     ptx::tc_fence_after();
                 }
+                TRACE(13);
 #pragma unroll
                 for (int cc = 0; cc < 4; ++cc) {
                     uint32_t pk[16];
@@ -328,13 +331,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                         ps[i & 3] += e0 + e1;
                         pk[i] = h2(e0, e1);
                     }
+#ifdef MKQ_ABL_NOST
+                    if (pk[0] == 0x12345678u && pk[15] == 0x9abcdef0u)
+#endif
                     tmem_st_x16(tP(x) + lane_off + 16 * cc, pk);
                 }
+#ifndef MKQ_ABL_NOSTAGGER
                 if (I.hasB) {
                     if (x == 0) ptx::named_bar_arrive(1 + q, 64);
                     if (x == 1 && j + 1 < I.nblk) ptx::named_bar_arrive(5 + q, 64);
                 }
+#endif
                 l += (ps[0] + ps[1]) + (ps[2] + ps[3]);
+                TRACE(14);
                 ptx::tmem_st_wait();
                 ptx::tc_fence_before();
                 __syncwarp();

@@ -126,27 +126,41 @@ __device__ __forceinline__ int out_pitch(int mode) {
 
 // 16 outputs (columns cl..cl+15 of one accumulator row) -> staging row `r`,
 // half `h2` of the 32-column block.
-__device__ __forceinline__ void epi2_half(const EpiParams& ep, const Lut& L, bool use_table, uint32_t scb,
+// scb holds (sc, b) per column with b = 0 without bias (fmaf(a, sc, +0) ==
+// fl32(a*sc) for sc > 0, R4) and, when `fold`, sc pre-multiplied by 2^-8:
+// fmaf((float)(256*sum), sc*2^-8, b) has the same exact product as
+// fmaf((float)sum, sc, b) (both scalings are exact: 256*sum is an integer
+// below 2^32 with >= 8 trailing zero bits, and sc*2^-8 is normal), so the
+// int4 scaling shift folds away.
+__device__ __forceinline__ void epi2_half(const EpiParams& ep, const Lut& L, bool use_table, bool fold, uint32_t scb,
                                           const uint32_t (&v)[16], uint8_t* stage, int r, int h2) {
-    int32_t acc[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) acc[i] = (int32_t)v[i] >> 8;
     const int mode = ep.mode;
     const int P = out_pitch(mode);
     if (mode == OUT_I32) {
+        int32_t acc[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) acc[i] = (int32_t)v[i] >> 8;
 #pragma unroll
         for (int c = 0; c < 4; ++c)
             *reinterpret_cast<int4*>(stage + stg_off(r, c, P)) =
                 make_int4(acc[4 * c], acc[4 * c + 1], acc[4 * c + 2], acc[4 * c + 3]);
         return;
     }
-    const bool hb = ep.bias != nullptr;
     float y[16];
+    if (fold) {
 #pragma unroll
-    for (int i = 0; i < 16; i += 2) {
-        const float4 sb = lds128f(scb + 8u * (uint32_t)i);   // (sc, b) of two columns, broadcast
-        y[i] = dequant(acc[i], sb.x, sb.y, hb);
-        y[i + 1] = dequant(acc[i + 1], sb.z, sb.w, hb);
+        for (int i = 0; i < 16; i += 2) {
+            const float4 sb = lds128f(scb + 8u * (uint32_t)i);   // (sc, b) of two columns, broadcast
+            y[i] = __fmaf_rn(__int2float_rn((int32_t)v[i]), sb.x, sb.y);
+            y[i + 1] = __fmaf_rn(__int2float_rn((int32_t)v[i + 1]), sb.z, sb.w);
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < 16; i += 2) {
+            const float4 sb = lds128f(scb + 8u * (uint32_t)i);
+            y[i] = __fmaf_rn(__int2float_rn((int32_t)v[i] >> 8), sb.x, sb.y);
+            y[i + 1] = __fmaf_rn(__int2float_rn((int32_t)v[i + 1] >> 8), sb.z, sb.w);
+        }
     }
     if (mode == OUT_I4 || mode == OUT_I8) {
         uint32_t q[16];
@@ -336,11 +350,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
             const int ab = it & 1;
             const uint32_t aph = (it >> 1) & 1;
             float2* sb = scb + ab * BN;
+            bool tiny = false;
+            float sc = 1.0f, bn = 0.0f;
             {   // per-column scale and bias of this tile
                 const int n = n0 + et;
-                if (et < BN && n < N)
-                    sb[et] = make_float2(__fmul_rn(ep.s_a, __ldg(ep.s_w + n)), ep.bias ? __ldg(ep.bias + n) : 0.0f);
+                if (et < BN && n < N) {
+                    sc = __fmul_rn(ep.s_a, __ldg(ep.s_w + n));
+                    bn = ep.bias ? __ldg(ep.bias + n) : 0.0f;
+                    tiny = !(sc >= 0x1p-118f);   // sc * 2^-8 would not be normal (or sc is not > 0)
+                }
             }
+            // fold the >> 8 into sc unless some column's sc is too small (rare; tile-uniform)
+            const bool fold = !ptx::named_bar_sync_or(1, kEpiThreads, tiny);
+            if (et < BN) sb[et] = make_float2(fold ? __fmul_rn(sc, 0x1p-8f) : sc, bn);
             ptx::named_bar_sync(1, kEpiThreads);
             ptx::mbar_wait(&tfull[ab], aph);
             ptx::tc_fence_after();
@@ -361,7 +383,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
                     uint32_t v[16];
                     ptx::tmem_ld_32x32b_x16(tmem_base + ((uint32_t)(q * 32) << 16) + ab * BN + cl + 16 * h2, v);
                     ptx::tmem_ld_wait();
-                    epi2_half(ep, L, use_table, ptx::smem_u32(sb + cl + 16 * h2), v, stage, lane, h2);
+                    epi2_half(ep, L, use_table, fold, ptx::smem_u32(sb + cl + 16 * h2), v, stage, lane, h2);
                     if (h2 == 1 || wide) {
                         ptx::fence_proxy_async_smem();
                         __syncwarp();
