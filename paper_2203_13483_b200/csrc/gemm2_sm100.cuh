@@ -36,8 +36,9 @@ struct Epi2Params {
     const void* table;   // rq table (global) or null
 };
 
-template <int BN_, int EPI_ = 8, int UNP_ = 8>
+template <int BN_, int EPI_ = 8, int UNP_ = 8, bool LUT4_ = false>
 struct Gemm2Cfg {
+    static constexpr bool kLut4 = LUT4_;             // int4 output through the compact requant table
     static constexpr int BM = 128;                  // A rows per CTA (MMA M = 256 per pair)
     static constexpr int BN = BN_;                  // MMA N (per pair)
     static constexpr int BNH = BN / 2;              // W rows per CTA
@@ -54,13 +55,16 @@ struct Gemm2Cfg {
     static constexpr int kUnpWarps = UNP_;          // 8 or 4
     static constexpr int kThreads = 32 * (4 + kEpiWarps + kUnpWarps);
     static constexpr uint32_t kTmemCols = 2 * BN;
-    static constexpr int kScb = 2 * BN * 8;          // 2 buffers x BN x (sc, b)
-    static constexpr int kStagePerWarp = 2048;      // 32 rows x 64 B output block per warp
-    static constexpr int kStaging = kEpiWarps * kStagePerWarp;
     static constexpr int kColsPerWarp = BN / (kEpiWarps / 4);
+    // (sc, b) per column: 2 tile buffers x BN (shared by the epilogue), or
+    // (kLut4) one private kColsPerWarp slice per epilogue warp
+    static constexpr int kScb = kLut4 ? kEpiWarps * kColsPerWarp * 8 : 2 * BN * 8;
+    static constexpr int kStagePerWarp = kLut4 ? 512 : 2048;   // 32 rows x 16 B (int4) / 64 B output block per warp
+    static constexpr int kStaging = kEpiWarps * kStagePerWarp;
+    static constexpr int kTabBytes = kLut4 ? (int)rq::kSmem4Bytes : (int)rq::kSmemBytes;
     static_assert(kColsPerWarp % 32 == 0, "epilogue column split");
     static constexpr int kBarBytes = 8 * (2 * S8 + 2 * SP + 4) + 16;
-    static constexpr int kSmem = 1024 + S8 * kStage8 + SP * kStageP + (int)rq::kSmemBytes + kScb + kStaging + kBarBytes;
+    static constexpr int kSmem = 1024 + S8 * kStage8 + SP * kStageP + kTabBytes + kScb + kStaging + kBarBytes;
     static_assert(kSmem <= 232448, "shared memory budget");
     static_assert(BN == 256 || BN == 128, "BN");
     static_assert((S8 * kStage8 + SP * kStageP) % 1024 == 0, "staging must be 1024-aligned (SWIZZLE_128B)");
@@ -97,7 +101,15 @@ __device__ __forceinline__ void lut_codes16(const Lut& L, const EpiParams& ep, c
     uint32_t any = 0;
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
+#if defined(MKQ_ABL_NOLUT)   // ablation (diagnostics only): no table load
+        const uint32_t ci = rq::cell_u(y[i], L.c0, L.inv_w, (uint32_t)L.ncell);
+        const uint2 e = make_uint2(ci << 20, ci);
+#elif defined(MKQ_ABL_LANELUT)   // ablation: conflict-free table addresses
+        const uint32_t ci = rq::cell_u(y[i], L.c0, L.inv_w, (uint32_t)L.ncell);
+        const uint2 e = lds64(L.cells + 8u * (((ci & 31u) << 5) | (threadIdx.x & 31u)));
+#else
         const uint2 e = lds64(L.cells + 8u * rq::cell_u(y[i], L.c0, L.inv_w, (uint32_t)L.ncell));
+#endif
         q[i] = __byte_perm(e.y, 0, y[i] >= __uint_as_float(e.x) ? 0x4441 : 0x4440);
         any |= e.y;
     }
@@ -212,6 +224,60 @@ __device__ __forceinline__ void epi2_half(const EpiParams& ep, const Lut& L, boo
     }
 }
 
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+
+// 32 int4 requantized codes of one accumulator row (columns cl..cl+31) through
+// the compact table (requant.cuh, "compact int4 table"): per output one cell
+// computation, one conflict-free 32-bit lookup (tab = this lane's replica),
+// one fp32 compare and a nibble insert; lanes within 511 ulps of a threshold
+// word, or any lane when the table is unusable, are evaluated directly.
+template <bool kFold>
+__device__ __forceinline__ void epi_lut4(const EpiParams& ep, const uint32_t (&v)[32], uint32_t scb, uint32_t tab,
+                                         float a4, float b4, bool tvalid, uint32_t (&w)[4]) {
+    uint32_t bad = tvalid ? 0xFFFFFFFFu : 0u;
+#pragma unroll
+    for (int i = 0; i < 32; i += 2) {
+        const float4 sb = lds128f(scb + 8u * (uint32_t)i);
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+            const int ii = i + t;
+            const int32_t acc = kFold ? (int32_t)v[ii] : ((int32_t)v[ii] >> 8);
+            const float y = __fmaf_rn(__int2float_rn(acc), t ? sb.z : sb.x, t ? sb.w : sb.y);
+#ifdef MKQ_ABL_L4NOLUT   // ablation (diagnostics only)
+            const uint32_t e = rq::cell4(y, a4, b4) * 0x01010101u;
+#else
+            const uint32_t e = lds32(tab + (rq::cell4(y, a4, b4) << 7));
+#endif
+            bad = min(bad, __float_as_uint(y) - e + 511u);
+            const bool ge = y >= __uint_as_float(e);
+            const int k = ii & 7;
+            if (k == 0) {
+                w[ii >> 3] = (e >> (ge ? 4 : 0)) & 0xFu;
+            } else {
+                w[ii >> 3] |= (e << (ge ? 4 * k - 4 : 4 * k)) & (0xFu << (4 * k));
+            }
+        }
+    }
+    if (__builtin_expect(__any_sync(0xffffffffu, bad < 1023u), 0)) {
+#pragma unroll
+        for (int ii = 0; ii < 32; ++ii) {
+            const uint2 sb = lds64(scb + 8u * (uint32_t)ii);
+            const int32_t acc = kFold ? (int32_t)v[ii] : ((int32_t)v[ii] >> 8);
+            const float y = __fmaf_rn(__int2float_rn(acc), __uint_as_float(sb.x), __uint_as_float(sb.y));
+            const uint32_t e = lds32(tab + (rq::cell4(y, a4, b4) << 7));
+            if (!tvalid || __float_as_uint(y) - e + 511u < 1023u) {
+                const uint32_t c = (uint32_t)requant_direct(y, ep.gelu, ep.s_out, ep.qmin, ep.qmax) & 0xFu;
+                const int k = ii & 7;
+                w[ii >> 3] = (w[ii >> 3] & ~(0xFu << (4 * k))) | (c << (4 * k));
+            }
+        }
+    }
+}
+
 template <class Cfg>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
     gemm_w4a4_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -226,7 +292,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
     uint8_t* staging = ringP + SP * Cfg::kStageP;   // 1024-aligned, 4 KB per epilogue warp
     rq::Header* th = reinterpret_cast<rq::Header*>(staging + Cfg::kStaging);
     uint2* tcells = reinterpret_cast<uint2*>(th + 1);
-    float2* scb = reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(th) + rq::kSmemBytes);
+    float2* scb = reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(th) + Cfg::kTabBytes);
     uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(scb) + Cfg::kScb);
     uint64_t* full8 = bars;
     uint64_t* empty8 = full8 + S8;
@@ -314,9 +380,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
                     ptx::tc_fence_after();
                     const uint64_t da = dA0 + (uint64_t)((s * Cfg::kStage8) >> 4);
                     const uint64_t db = da + (uint64_t)(Cfg::kA8 >> 4);
+#ifndef MKQ_ABL_NOMMA
 #pragma unroll
                     for (int k = 0; k < Cfg::BK / 32; ++k)
                         ptx::mma_i8_ss_2cta_warp(d, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+#endif
                     ptx::mma_commit_2cta_mc_warp(&empty8[s], 3);
                     if (++s == S8) { s = 0; ph ^= 1; }
                 }
@@ -330,13 +398,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
         const int h = e >> 2;             // column part (kColsPerWarp columns)
         const int et = threadIdx.x - 128; // 0..255
         bool use_table = false;
-        if (p.table) {
+        float a4 = 0.0f, b4 = 0.0f;
+        if constexpr (Cfg::kLut4) {
+            // replicate each compact-table word 32 times (word c*32 + l for lane l)
+            const uint8_t* tg = reinterpret_cast<const uint8_t*>(p.table);
+            const rq::Header* hg = reinterpret_cast<const rq::Header*>(tg);
+            const rq::Header4* h4 = reinterpret_cast<const rq::Header4*>(tg + rq::kOff4);
+            const uint32_t* c4 = reinterpret_cast<const uint32_t*>(h4 + 1);
+            uint32_t* dst = reinterpret_cast<uint32_t*>(th);
+            for (int i = et; i < rq::kCells4 * 32; i += kEpiThreads) dst[i] = __ldg(c4 + (i >> 5));
+            use_table = h4->valid != 0 && hg->gelu == ep.gelu && hg->s_out == ep.s_out && hg->qmin == ep.qmin &&
+                        hg->qmax == ep.qmax;
+            a4 = h4->a;
+            b4 = h4->b;
+        } else if (p.table) {
             const uint32_t* src = reinterpret_cast<const uint32_t*>(p.table);
             uint32_t* dst = reinterpret_cast<uint32_t*>(th);
             for (int i = et; i < (int)(rq::kSmemBytes / 4); i += kEpiThreads) dst[i] = src[i];
         }
         ptx::named_bar_sync(1, kEpiThreads);
-        if (p.table)
+        if (!Cfg::kLut4 && p.table)
             use_table = th->valid != 0 && th->gelu == ep.gelu && th->s_out == ep.s_out && th->qmin == ep.qmin &&
                         th->qmax == ep.qmax;
         Lut L{0.0f, 0.0f, 1, ptx::smem_u32(tcells)};
@@ -350,6 +431,68 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
             const int ab = it & 1;
             const uint32_t aph = (it >> 1) & 1;
             float2* sb = scb + ab * BN;
+            if constexpr (Cfg::kLut4) {
+                // per-warp (sc, b) of this warp's kColsPerWarp columns: no epilogue-wide
+                // barrier per tile, warps slip freely against each other
+                float2* wsb = scb + e * Cfg::kColsPerWarp;
+                const int cw = n0 + h * Cfg::kColsPerWarp;
+                float2 v2[Cfg::kColsPerWarp / 32];
+                bool ok = true;
+#pragma unroll
+                for (int c = 0; c < Cfg::kColsPerWarp / 32; ++c) {
+                    const int n = cw + 32 * c + lane;
+                    float sc = 1.0f, bn = 0.0f;
+                    if (n < N) {
+                        sc = __fmul_rn(ep.s_a, __ldg(ep.s_w + n));
+                        bn = ep.bias ? __ldg(ep.bias + n) : 0.0f;
+                        ok = ok && sc >= 0x1p-118f;
+                    }
+                    v2[c] = make_float2(sc, bn);
+                }
+                const bool wfold = __all_sync(0xffffffffu, ok);
+                __syncwarp();
+#pragma unroll
+                for (int c = 0; c < Cfg::kColsPerWarp / 32; ++c)
+                    wsb[32 * c + lane] = make_float2(wfold ? __fmul_rn(v2[c].x, 0x1p-8f) : v2[c].x, v2[c].y);
+                __syncwarp();
+                ptx::mbar_wait(&tfull[ab], aph);
+                ptx::tc_fence_after();
+                const int row0 = m0 + q * 32;
+                const uint32_t tab = ptx::smem_u32(th) + 4u * (uint32_t)lane;
+#pragma unroll 1
+                for (int j = 0; j < Cfg::kColsPerWarp / 32; ++j) {
+                    const int cl = h * Cfg::kColsPerWarp + 32 * j;
+                    const int n = n0 + cl;
+                    if (n >= N) break;
+#ifdef MKQ_ABL_NOEPI
+                    break;
+#endif
+                    if (lane == 0) ptx::tma_store_wait_read<0>();
+                    __syncwarp();
+                    uint32_t v[32];
+                    ptx::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + ab * BN + cl, v);
+                    ptx::tmem_ld_wait();
+                    uint32_t w[4];
+                    const uint32_t sba = ptx::smem_u32(wsb + 32 * j);
+                    if (wfold)
+                        epi_lut4<true>(ep, v, sba, tab, a4, b4, use_table, w);
+                    else
+                        epi_lut4<false>(ep, v, sba, tab, a4, b4, use_table, w);
+                    *reinterpret_cast<uint4*>(stage + lane * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+                    ptx::fence_proxy_async_smem();
+                    __syncwarp();
+#ifndef MKQ_ABL_L4NOSTORE
+                    if (lane == 0) {
+                        ptx::tma_store_2d(&tmO, stage, n / 2, row0);
+                        ptx::tma_store_commit();
+                    }
+#endif
+                }
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive_remote(ptx::mapa(&tempty[ab], 0));
+                continue;
+            }
             bool tiny = false;
             float sc = 1.0f, bn = 0.0f;
             {   // per-column scale and bias of this tile
@@ -367,6 +510,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
             ptx::mbar_wait(&tfull[ab], aph);
             ptx::tc_fence_after();
             const int row0 = m0 + q * 32;
+            {
 #pragma unroll 1
             for (int j = 0; j < Cfg::kColsPerWarp / 32; ++j) {
                 const int cl = h * Cfg::kColsPerWarp + 32 * j;
@@ -394,6 +538,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
                         }
                     }
                 }
+            }
             }
             ptx::tc_fence_before();
             __syncwarp();

@@ -279,7 +279,10 @@ mkq_status gemm_common(bool int4, const void* a, int64_t lda, const void* w, int
         // unpack warps; longer K keeps 8 + 8 (mainloop-bound)
         static const int epi_override = [] { const char* v = getenv("MKQ_EPI_WARPS"); return v ? atoi(v) : 0; }();
         const bool many_epi = epi_override ? epi_override == 16 : K <= 1024;
+        static const bool no_lut4 = getenv("MKQ_NO_LUT4") != nullptr;   // diagnostics
         if (N % 256 == 0) {
+            if (many_epi && e.out == MKQ_OUT_I4 && p2.table && !no_lut4)
+                return launch_gemm2<mkq::Gemm2Cfg<256, 16, 4, true>>(a, lda, w, ldw, (int)M, (int)N, (int)K, p2, sms, st);
             if (many_epi)
                 return launch_gemm2<mkq::Gemm2Cfg<256, 16, 4>>(a, lda, w, ldw, (int)M, (int)N, (int)K, p2, sms, st);
             return launch_gemm2<mkq::Gemm2Cfg<256>>(a, lda, w, ldw, (int)M, (int)N, (int)K, p2, sms, st);
@@ -466,12 +469,16 @@ mkq_status mkq_requant_table(int gelu, float s_out, int qmin, int qmax, void* ta
     const uint32_t np = bh - bz + 1, nn = bl - bz + 1;
     Header* h = static_cast<Header*>(table);
     uint2* cells = reinterpret_cast<uint2*>(h + 1);
-    Change* chg = reinterpret_cast<Change*>(static_cast<uint8_t*>(table) + sizeof(Header) + kCells * 8);
+    Header4* h4 = reinterpret_cast<Header4*>(static_cast<uint8_t*>(table) + kOff4);
+    uint32_t* cells4 = reinterpret_cast<uint32_t*>(h4 + 1);
+    Change* chg = reinterpret_cast<Change*>(reinterpret_cast<uint8_t*>(cells4) + kCells4 * 4);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     init_kernel<<<1, 1, 0, st>>>(h, y_lo, y_hi, inv_w, y_zero, kCells, code_lo, code_hi, gelu, qmin, qmax, s_out);
     scan_kernel<<<sms * 8, 256, 0, st>>>(h, chg, bz, np, bz, nn);
     finalize_kernel<<<1, 32, 0, st>>>(h, cells, chg);
     verify_kernel<<<sms * 8, 256, 0, st>>>(h, cells, bz, np, bz, nn);
+    finalize4_kernel<<<1, 32, 0, st>>>(h, h4, cells4, chg);
+    verify4_kernel<<<sms * 8, 256, 0, st>>>(h, h4, cells4, bz, np, bz, nn);
     cudaError_t e = cudaPeekAtLastError();
     return e == cudaSuccess ? MKQ_OK : cuda_fail(e, "requant table launch");
 }

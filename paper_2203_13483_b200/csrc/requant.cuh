@@ -43,9 +43,48 @@ struct Change {
     int before, after, pad;
 };
 
-// table bytes: header + cells (uint2: thr bits, meta) + change scratch
-constexpr size_t kTableBytes = sizeof(Header) + kCells * 8 + kMaxChanges * sizeof(Change);
+// ---- compact int4 table (the FFN1 epilogue's fast path; int4 outputs only)
+// 256 cells over the span of the change points, one 32-bit word per cell:
+//     cell(y) = cvt.rmi.u32( fl( sat(fma(y, a, b)) * 255 ) )        in [0, 255]
+//     word    = (bits(thr) & ~0x1FF) | below | above << 4            (>= 1 change)
+//             = 0x7F800000 | below | below << 4  (NaN: y >= it is false)  (none)
+// The low 9 bits of the threshold are given up for the two nibbles, so the
+// fp32 compare  y >= float(word)  decides exactly except for y within 511 ulps
+// of the word; the epilogue detects those lanes with one integer test
+// (bits(y) - word + 511 < 1023, unsigned) and evaluates them directly.  A
+// table needing two change points in one cell is marked invalid.  In shared
+// memory each word is replicated 32 times (lane l reads bank l), so a warp's
+// 32 lookups are one conflict-free wavefront.
+constexpr int kCells4 = 256;
+struct Header4 {
+    float a, b;
+    int valid, pad[13];
+};   // 64 bytes
+
+// table bytes: header + cells (uint2: thr bits, meta) + header4 + cells4 + change scratch
+constexpr size_t kOff4 = sizeof(Header) + kCells * 8;
+constexpr size_t kTableBytes = kOff4 + sizeof(Header4) + kCells4 * 4 + kMaxChanges * sizeof(Change);
 constexpr size_t kSmemBytes = sizeof(Header) + kCells * 8;
+constexpr size_t kSmem4Bytes = kCells4 * 32 * 4;   // replicated cells4
+
+__device__ __forceinline__ float fma_sat(float x, float a, float b) {
+    float r;
+    asm("fma.rn.sat.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(x), "f"(a), "f"(b));
+    return r;
+}
+// cell of the compact table: the epilogue's exact sequence
+__device__ __forceinline__ uint32_t cell4(float y, float a, float b) {
+    uint32_t i;
+    asm("cvt.rmi.u32.f32 %0, %1;" : "=r"(i) : "f"(__fmul_rn(fma_sat(y, a, b), 255.0f)));
+    return i;
+}
+// 0 = decided: *code = the int4 field; 1 = y is within 511 ulps of the
+// cell's threshold word (evaluate directly)
+__device__ __forceinline__ bool lookup4(uint32_t w, float y, uint32_t* field) {
+    if (__float_as_uint(y) - w + 511u < 1023u) return true;
+    *field = (y >= __uint_as_float(w) ? (w >> 4) : w) & 0xFu;
+    return false;
+}
 
 __device__ __forceinline__ int direct_code(float y, int gelu, float s, int qmin, int qmax) {
     return quant_code(gelu ? gelu_pinned(y) : y, s, qmin, qmax);
@@ -166,6 +205,60 @@ __global__ void finalize_kernel(Header* h, uint2* cells, Change* chg) {
     }
     if (run != h->code_hi || p != n) ok = false;
     h->valid = ok ? 1 : 0;
+}
+
+// compact table from the sorted change list (run after finalize_kernel)
+__global__ void finalize4_kernel(Header* h, Header4* h4, uint32_t* cells4, const Change* chg) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    Header4 v{};
+    const int n = h->nchg;
+    bool ok = is_int4(h->qmin, h->qmax) && n <= kMaxChanges;
+    if (n >= 2) {
+        const float lo = chg[0].y, hi = chg[n - 1].y;
+        v.a = __fdiv_rn(1.0f, hi - lo);
+        v.b = __fmaf_rn(-lo, v.a, 0.5f / 255.0f);
+    } else if (n == 1) {
+        v.a = 1.0f;
+        v.b = __fadd_rn(0.5f, -chg[0].y);
+    }
+    if (!(v.a >= 0.0f && v.a < 3.0e38f)) ok = false;
+    int run = h->code_lo;
+    int p = 0;
+    for (int i = 0; i < kCells4 && ok; ++i) {
+        uint32_t w = 0x7F800000u | (uint32_t)(run & 0xF) * 0x11u;
+        int cnt = 0;
+        while (p < n && (int)cell4(chg[p].y, v.a, v.b) == i) {
+            if (chg[p].before != run) ok = false;
+            w = (__float_as_uint(chg[p].y) & ~0x1FFu) | (uint32_t)(run & 0xF) | ((uint32_t)(chg[p].after & 0xF) << 4);
+            run = chg[p].after;
+            ++cnt;
+            ++p;
+        }
+        if (cnt > 1) ok = false;
+        cells4[i] = w;
+    }
+    if (run != h->code_hi || p != n) ok = false;
+    v.valid = ok ? 1 : 0;
+    *h4 = v;
+}
+
+// every float of the scanned ranges: lookup4 decision == direct evaluation
+__global__ void verify4_kernel(const Header* h, Header4* h4, const uint32_t* cells4, uint32_t bp0, uint32_t np,
+                               uint32_t bn0, uint32_t nn) {
+    if (!h4->valid) return;
+    const float a = h4->a, b = h4->b;
+    const int gelu = h->gelu, qmin = h->qmin, qmax = h->qmax;
+    const float s = h->s_out;
+    const uint32_t total = np + nn;
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < total; k += gridDim.x * blockDim.x) {
+        const float y = k < np ? range_y(0, bp0, np, k) : range_y(1, bn0, nn, k - np);
+        uint32_t f;
+        if (lookup4(cells4[cell4(y, a, b)], y, &f)) continue;
+        if (f != ((uint32_t)direct_code(y, gelu, s, qmin, qmax) & 0xFu)) {
+            h4->valid = 0;
+            return;
+        }
+    }
 }
 
 __global__ void verify_kernel(Header* h, const uint2* cells, uint32_t bp0, uint32_t np, uint32_t bn0, uint32_t nn) {

@@ -244,6 +244,8 @@ def test_requant_table_bitexact(gelu, s_out, bits):
     tab = M.mkq_requant_table(gelu, s_out, lo, hi, DEV, cache=False)
     torch.cuda.synchronize()
     assert int(tab[28:32].view(torch.int32).item()) == 1, "table self-verification failed"
+    if bits == 4 and s_out >= 0.05:   # the compact int4 table (FFN1 fast path) must be usable too
+        assert int(tab[TAB4 + 8:TAB4 + 12].view(torch.int32).item()) == 1, "compact table not valid"
     rng = np.random.default_rng(int(s_out * 1000) + bits)
     Mm, N, K = 1000, 1024, 1024
     A, W = _codes(rng, Mm, N, K, bits)
@@ -259,6 +261,37 @@ def test_requant_table_bitexact(gelu, s_out, bits):
     ref = oracle.linear(A, W, s_a, s_w, b, mode=oracle.OUT_I4 if bits == 4 else oracle.OUT_I8, gelu=gelu,
                         s_out=np.float32(s_out), qmin_out=lo, qmax_out=hi)
     assert np.array_equal(with_t if bits == 4 else with_t.view(np.int8), oracle.pack_int4(ref) if bits == 4 else ref)
+
+
+TAB4 = 64 + 1024 * 8   # byte offset of the compact int4 table header (requant.cuh kOff4)
+
+
+@pytest.mark.parametrize("s_out", [0.36, 0.05])
+def test_requant_table4_threshold_neighbourhoods(s_out):
+    """The compact table gives up the low 9 bits of each threshold: drive y
+    through +-600 ulps around every threshold word (acc = 0, so y = bias
+    exactly) and through the non-folded (tiny scale) epilogue; every code
+    must equal the oracle's direct evaluation."""
+    tab = M.mkq_requant_table(True, s_out, -8, 7, DEV, cache=False)
+    torch.cuda.synchronize()
+    t = tab.cpu().numpy()
+    assert t[TAB4 + 8:TAB4 + 12].view(np.int32)[0] == 1
+    words = t[TAB4 + 64:TAB4 + 64 + 256 * 4].view(np.uint32)
+    thr = words[(words & 0x7F800000) != 0x7F800000]
+    assert thr.size >= 5
+    ys = np.unique(np.concatenate([(w.astype(np.int64) + np.arange(-600, 601)) for w in thr]).astype(np.uint32))
+    ys = ys.view(np.float32)
+    N = (ys.size + 255) // 256 * 256
+    b = np.resize(ys, N).astype(np.float32)
+    rng = np.random.default_rng(11)
+    K = 256
+    A = np.zeros((256, K), np.int8)
+    W = rng.integers(-7, 8, (N, K)).astype(np.int8)
+    s_w = np.full(N, 2e-3, np.float32)
+    s_w[N // 2: N // 2 + 256] = 1e-37   # one tile with an unfoldable (tiny) scale
+    out = host(_run(4, A, W, np.float32(0.3), s_w, b, mode=M.OUT_I4, gelu=True, s_out=s_out, requant_table=tab))
+    ref = oracle.linear(A, W, np.float32(0.3), s_w, b, mode=oracle.OUT_I4, gelu=True, s_out=np.float32(s_out))
+    assert np.array_equal(out, oracle.pack_int4(ref))
 
 
 def test_requant_table_mismatched_params_ignored():
