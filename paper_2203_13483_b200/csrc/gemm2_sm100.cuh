@@ -230,44 +230,60 @@ __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
     return v;
 }
 
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {   // two IEEE RN fmas, one instruction
+    uint64_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;"
+        : "=l"(r)
+        : "l"(*reinterpret_cast<const uint64_t*>(&a)), "l"(*reinterpret_cast<const uint64_t*>(&b)),
+          "l"(*reinterpret_cast<const uint64_t*>(&c)));
+    return *reinterpret_cast<float2*>(&r);
+}
+
 // 32 int4 requantized codes of one accumulator row (columns cl..cl+31) through
 // the compact table (requant.cuh, "compact int4 table"): per output one cell
 // computation, one conflict-free 32-bit lookup (tab = this lane's replica),
 // one fp32 compare and a nibble insert; lanes within 511 ulps of a threshold
 // word, or any lane when the table is unusable, are evaluated directly.
+// scb: (sc, sc', b, b') per column pair, so the dequant fma runs as f32x2.
 template <bool kFold>
 __device__ __forceinline__ void epi_lut4(const EpiParams& ep, const uint32_t (&v)[32], uint32_t scb, uint32_t tab,
                                          float a4, float b4, bool tvalid, uint32_t (&w)[4]) {
     uint32_t bad = tvalid ? 0xFFFFFFFFu : 0u;
+    const uint32_t tabm = tab - (rq::kMagic << 7);   // (bits - magic) * 128 + tab, mod 2^32
 #pragma unroll
     for (int i = 0; i < 32; i += 2) {
         const float4 sb = lds128f(scb + 8u * (uint32_t)i);
+        const int32_t a0 = kFold ? (int32_t)v[i] : ((int32_t)v[i] >> 8);
+        const int32_t a1 = kFold ? (int32_t)v[i + 1] : ((int32_t)v[i + 1] >> 8);
+        const float2 y = fma2(make_float2(__int2float_rn(a0), __int2float_rn(a1)), make_float2(sb.x, sb.y),
+                              make_float2(sb.z, sb.w));
+        const float2 cf = fma2(make_float2(rq::fma_sat(y.x, a4, b4), rq::fma_sat(y.y, a4, b4)),
+                               make_float2(255.0f, 255.0f), make_float2(8388608.0f, 8388608.0f));
 #pragma unroll
         for (int t = 0; t < 2; ++t) {
             const int ii = i + t;
-            const int32_t acc = kFold ? (int32_t)v[ii] : ((int32_t)v[ii] >> 8);
-            const float y = __fmaf_rn(__int2float_rn(acc), t ? sb.z : sb.x, t ? sb.w : sb.y);
+            const float yy = t ? y.y : y.x;
 #ifdef MKQ_ABL_L4NOLUT   // ablation (diagnostics only)
-            const uint32_t e = rq::cell4(y, a4, b4) * 0x01010101u;
+            const uint32_t e = __float_as_uint(t ? cf.y : cf.x) * 0x01010101u;
 #else
-            const uint32_t e = lds32(tab + (rq::cell4(y, a4, b4) << 7));
+            const uint32_t e = lds32(__float_as_uint(t ? cf.y : cf.x) * 128u + tabm);
 #endif
-            bad = min(bad, __float_as_uint(y) - e + 511u);
-            const bool ge = y >= __uint_as_float(e);
+            bad = min(bad, __float_as_uint(yy) - e + 511u);
+            const uint32_t f = yy >= __uint_as_float(e) ? (e >> 4) : e;
             const int k = ii & 7;
-            if (k == 0) {
-                w[ii >> 3] = (e >> (ge ? 4 : 0)) & 0xFu;
-            } else {
-                w[ii >> 3] |= (e << (ge ? 4 * k - 4 : 4 * k)) & (0xFu << (4 * k));
-            }
+            if (k == 0)
+                w[ii >> 3] = f & 0xFu;
+            else
+                w[ii >> 3] |= (f << (4 * k)) & (0xFu << (4 * k));
         }
     }
     if (__builtin_expect(__any_sync(0xffffffffu, bad < 1023u), 0)) {
 #pragma unroll
         for (int ii = 0; ii < 32; ++ii) {
-            const uint2 sb = lds64(scb + 8u * (uint32_t)ii);
+            const uint32_t pb = scb + 16u * (uint32_t)(ii >> 1) + 4u * (uint32_t)(ii & 1);
+            const float sc = __uint_as_float(lds32(pb)), bb = __uint_as_float(lds32(pb + 8u));
             const int32_t acc = kFold ? (int32_t)v[ii] : ((int32_t)v[ii] >> 8);
-            const float y = __fmaf_rn(__int2float_rn(acc), __uint_as_float(sb.x), __uint_as_float(sb.y));
+            const float y = __fmaf_rn(__int2float_rn(acc), sc, bb);
             const uint32_t e = lds32(tab + (rq::cell4(y, a4, b4) << 7));
             if (!tvalid || __float_as_uint(y) - e + 511u < 1023u) {
                 const uint32_t c = (uint32_t)requant_direct(y, ep.gelu, ep.s_out, ep.qmin, ep.qmax) & 0xFu;
@@ -453,7 +469,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
                 __syncwarp();
 #pragma unroll
                 for (int c = 0; c < Cfg::kColsPerWarp / 32; ++c)
-                    wsb[32 * c + lane] = make_float2(wfold ? __fmul_rn(v2[c].x, 0x1p-8f) : v2[c].x, v2[c].y);
+                {   // layout per column pair: (sc_even, sc_odd, b_even, b_odd)
+                    const int col = 32 * c + lane;
+                    float* f = reinterpret_cast<float*>(wsb) + 4 * (col >> 1) + (col & 1);
+                    f[0] = wfold ? __fmul_rn(v2[c].x, 0x1p-8f) : v2[c].x;
+                    f[2] = v2[c].y;
+                }
                 __syncwarp();
                 ptx::mbar_wait(&tfull[ab], aph);
                 ptx::tc_fence_after();

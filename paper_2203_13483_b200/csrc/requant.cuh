@@ -45,7 +45,7 @@ struct Change {
 
 // ---- compact int4 table (the FFN1 epilogue's fast path; int4 outputs only)
 // 256 cells over the span of the change points, one 32-bit word per cell:
-//     cell(y) = cvt.rmi.u32( fl( sat(fma(y, a, b)) * 255 ) )        in [0, 255]
+//     cell(y) = RN(255 * sat(fma(y, a, b)))  in [0, 255]   (cell4 below)
 //     word    = (bits(thr) & ~0x1FF) | below | above << 4            (>= 1 change)
 //             = 0x7F800000 | below | below << 4  (NaN: y >= it is false)  (none)
 // The low 9 bits of the threshold are given up for the two nibbles, so the
@@ -72,11 +72,12 @@ __device__ __forceinline__ float fma_sat(float x, float a, float b) {
     asm("fma.rn.sat.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(x), "f"(a), "f"(b));
     return r;
 }
-// cell of the compact table: the epilogue's exact sequence
+// cell of the compact table, the epilogue's exact sequence: u = sat(fma(y, a, b))
+// in [0, 1], then fma(u, 255, 2^23) lies in [2^23, 2^23 + 255] where the ulp is
+// 1, so its mantissa is the cell RN(255 u) (no float->int conversion).
+constexpr uint32_t kMagic = 0x4B000000u;   // bits of 2^23
 __device__ __forceinline__ uint32_t cell4(float y, float a, float b) {
-    uint32_t i;
-    asm("cvt.rmi.u32.f32 %0, %1;" : "=r"(i) : "f"(__fmul_rn(fma_sat(y, a, b), 255.0f)));
-    return i;
+    return __float_as_uint(__fmaf_rn(fma_sat(y, a, b), 255.0f, 8388608.0f)) - kMagic;
 }
 // 0 = decided: *code = the int4 field; 1 = y is within 511 ulps of the
 // cell's threshold word (evaluate directly)
