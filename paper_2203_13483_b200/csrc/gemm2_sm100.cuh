@@ -224,6 +224,25 @@ __device__ __forceinline__ void epi2_half(const EpiParams& ep, const Lut& L, boo
     }
 }
 
+#ifdef MKQ_GTRACE
+// Diagnostics build only (tools/trace_gemm.py): per-warp (tag, clock64) event
+// log of CTA 0 of the 2-CTA GEMM.
+__device__ unsigned long long* g_gtrace = nullptr;
+constexpr int kGTraceSlots = 512;
+#define GTRACE(tag)                                                                                    \
+    do {                                                                                               \
+        if (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && g_gtrace && gt_n < kGTraceSlots) {          \
+            g_gtrace[(threadIdx.x >> 5) * kGTraceSlots * 2 + 2 * gt_n] = (tag);                         \
+            g_gtrace[(threadIdx.x >> 5) * kGTraceSlots * 2 + 2 * gt_n + 1] = clock64();                 \
+            ++gt_n;                                                                                    \
+        }                                                                                              \
+    } while (0)
+#else
+#define GTRACE(tag) \
+    do {            \
+    } while (0)
+#endif
+
 __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
     uint32_t v;
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
@@ -250,32 +269,44 @@ __device__ __forceinline__ void epi_lut4(const EpiParams& ep, const uint32_t (&v
                                          float a4, float b4, bool tvalid, uint32_t (&w)[4]) {
     uint32_t bad = tvalid ? 0xFFFFFFFFu : 0u;
     const uint32_t tabm = tab - (rq::kMagic << 7);   // (bits - magic) * 128 + tab, mod 2^32
+    // phase 1: y for all 32 outputs (dequant as f32x2), phase 2: all 32 cell
+    // addresses and table loads in flight, phase 3: the decisions
+    float y[32];
 #pragma unroll
     for (int i = 0; i < 32; i += 2) {
         const float4 sb = lds128f(scb + 8u * (uint32_t)i);
         const int32_t a0 = kFold ? (int32_t)v[i] : ((int32_t)v[i] >> 8);
         const int32_t a1 = kFold ? (int32_t)v[i + 1] : ((int32_t)v[i + 1] >> 8);
-        const float2 y = fma2(make_float2(__int2float_rn(a0), __int2float_rn(a1)), make_float2(sb.x, sb.y),
-                              make_float2(sb.z, sb.w));
-        const float2 cf = fma2(make_float2(rq::fma_sat(y.x, a4, b4), rq::fma_sat(y.y, a4, b4)),
-                               make_float2(255.0f, 255.0f), make_float2(8388608.0f, 8388608.0f));
+        const float2 yy = fma2(make_float2(__int2float_rn(a0), __int2float_rn(a1)), make_float2(sb.x, sb.y),
+                               make_float2(sb.z, sb.w));
+        y[i] = yy.x;
+        y[i + 1] = yy.y;
+    }
+    uint32_t e[32];
 #pragma unroll
-        for (int t = 0; t < 2; ++t) {
-            const int ii = i + t;
-            const float yy = t ? y.y : y.x;
+    for (int i = 0; i < 32; i += 2) {
+        const float2 cf = fma2(make_float2(rq::fma_sat(y[i], a4, b4), rq::fma_sat(y[i + 1], a4, b4)),
+                               make_float2(255.0f, 255.0f), make_float2(8388608.0f, 8388608.0f));
+        e[i] = __float_as_uint(cf.x) * 128u + tabm;
+        e[i + 1] = __float_as_uint(cf.y) * 128u + tabm;
+    }
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
 #ifdef MKQ_ABL_L4NOLUT   // ablation (diagnostics only)
-            const uint32_t e = __float_as_uint(t ? cf.y : cf.x) * 0x01010101u;
+        e[i] = e[i] * 0x01010101u;
 #else
-            const uint32_t e = lds32(__float_as_uint(t ? cf.y : cf.x) * 128u + tabm);
+        e[i] = lds32(e[i]);
 #endif
-            bad = min(bad, __float_as_uint(yy) - e + 511u);
-            const uint32_t f = yy >= __uint_as_float(e) ? (e >> 4) : e;
-            const int k = ii & 7;
-            if (k == 0)
-                w[ii >> 3] = f & 0xFu;
-            else
-                w[ii >> 3] |= (f << (4 * k)) & (0xFu << (4 * k));
-        }
+    }
+#pragma unroll
+    for (int ii = 0; ii < 32; ++ii) {
+        bad = min(bad, __float_as_uint(y[ii]) - e[ii] + 511u);
+        const uint32_t f = y[ii] >= __uint_as_float(e[ii]) ? (e[ii] >> 4) : e[ii];
+        const int k = ii & 7;
+        if (k == 0)
+            w[ii >> 3] = f & 0xFu;
+        else
+            w[ii >> 3] |= (f << (4 * k)) & (0xFu << (4 * k));
     }
     if (__builtin_expect(__any_sync(0xffffffffu, bad < 1023u), 0)) {
 #pragma unroll
@@ -319,6 +350,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
     const EpiParams& ep = p.e;
+#ifdef MKQ_GTRACE
+    int gt_n = 0;
+#endif
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const uint32_t rank = ptx::cluster_ctarank();
@@ -356,7 +390,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
     __syncthreads();   // CTA barrier as well (orders the slot write for tools that do not model barrier.cluster)
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-
+    // kLut4: register reallocation per warpgroup (each executes one setmaxnreg
+    // at one PC): producer/MMA group 40, unpack 56, epilogue (the latency-bound
+    // role) the rest of the launch allocation (80 x 768), 96
+    if (warp < 4) {
+    if constexpr (Cfg::kLut4) asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
     if (warp == 0) {
         // ---------------------------------------------------- TMA producer (both CTAs)
         if (lane == 0) {
@@ -388,11 +426,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
             for (int tile = cluster; tile < num_tiles; tile += nclusters, ++it) {
                 const int ab = it & 1;
                 const uint32_t aph = (it >> 1) & 1;
+                GTRACE(29);
                 ptx::mbar_wait(&tempty[ab], aph ^ 1);
+                GTRACE(30);
                 ptx::tc_fence_after();
                 const uint32_t d = tmem_base + ab * BN;
                 for (int kb = 0; kb < nk; ++kb) {
                     ptx::mbar_wait(&full8[s], ph);
+                    GTRACE(31);
                     ptx::tc_fence_after();
                     const uint64_t da = dA0 + (uint64_t)((s * Cfg::kStage8) >> 4);
                     const uint64_t db = da + (uint64_t)(Cfg::kA8 >> 4);
@@ -407,7 +448,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
                 ptx::mma_commit_2cta_mc_warp(&tfull[ab], 3);
             }
         }
-    } else if (warp >= 4 && warp < 4 + Cfg::kEpiWarps) {
+    }
+    } else if (warp < 4 + Cfg::kEpiWarps) {
+        if constexpr (Cfg::kLut4) asm volatile("setmaxnreg.inc.sync.aligned.u32 96;");
         // ---------------------------------------------------- epilogue (both CTAs)
         const int e = warp - 4;           // 0..7
         const int q = warp & 3;           // TMEM lane quadrant (warp % 4)
@@ -465,6 +508,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
                     }
                     v2[c] = make_float2(sc, bn);
                 }
+                GTRACE(1);
                 const bool wfold = __all_sync(0xffffffffu, ok);
                 __syncwarp();
 #pragma unroll
@@ -476,7 +520,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
                     f[2] = v2[c].y;
                 }
                 __syncwarp();
+                GTRACE(2);
                 ptx::mbar_wait(&tfull[ab], aph);
+                GTRACE(3);
                 ptx::tc_fence_after();
                 const int row0 = m0 + q * 32;
                 const uint32_t tab = ptx::smem_u32(th) + 4u * (uint32_t)lane;
@@ -490,15 +536,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
 #endif
                     if (lane == 0) ptx::tma_store_wait_read<0>();
                     __syncwarp();
+                    GTRACE(4);
                     uint32_t v[32];
                     ptx::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + ab * BN + cl, v);
                     ptx::tmem_ld_wait();
+                    GTRACE(5);
                     uint32_t w[4];
                     const uint32_t sba = ptx::smem_u32(wsb + 32 * j);
                     if (wfold)
                         epi_lut4<true>(ep, v, sba, tab, a4, b4, use_table, w);
                     else
                         epi_lut4<false>(ep, v, sba, tab, a4, b4, use_table, w);
+                    GTRACE(6);
                     *reinterpret_cast<uint4*>(stage + lane * 16) = make_uint4(w[0], w[1], w[2], w[3]);
                     ptx::fence_proxy_async_smem();
                     __syncwarp();
@@ -512,6 +561,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive_remote(ptx::mapa(&tempty[ab], 0));
+                GTRACE(8);
                 continue;
             }
             bool tiny = false;
@@ -566,7 +616,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
             if (lane == 0) ptx::mbar_arrive_remote(ptx::mapa(&tempty[ab], 0));
         }
         if (lane == 0) ptx::tma_store_wait<0>();
-    } else if (warp >= 4 + Cfg::kEpiWarps) {
+    } else {
+        if constexpr (Cfg::kLut4) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
         // ---------------------------------------------------- int4 -> int8 unpack (both CTAs)
         const int u = threadIdx.x - 32 * (4 + Cfg::kEpiWarps);
         constexpr int kChunks = (BM + BNH) * (Cfg::BK / 32);   // 16-byte packed chunks per stage
@@ -584,7 +635,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
         uint32_t php = 0, ph8 = 0;
         for (int tile = cluster; tile < num_tiles; tile += nclusters) {
             for (int kb = 0; kb < nk; ++kb) {
+                GTRACE(19);
                 ptx::mbar_wait(&fullP[sp], php);
+                GTRACE(20);
                 const uint32_t src = ringP_s + (uint32_t)sp * Cfg::kStageP + src_off;
                 uint4 pk[kPer];
 #ifndef MKQ_DBG_NO_UNPACK
@@ -592,6 +645,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
                 for (int i = 0; i < kPer; ++i) pk[i] = ptx::lds128(src + (uint32_t)i * (kRowsPerPass * 64u));
 #endif
                 ptx::mbar_wait(&empty8[s8], ph8 ^ 1);
+                GTRACE(21);
                 const uint32_t dst = ring8_s + (uint32_t)s8 * Cfg::kStage8;
 #ifndef MKQ_DBG_NO_UNPACK
 #pragma unroll
@@ -637,3 +691,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
 }
 
 }  // namespace mkq
+
+#ifdef MKQ_GTRACE
+extern "C" __attribute__((visibility("default"))) int mkq_debug_set_gtrace(void* p) {
+    unsigned long long* q = static_cast<unsigned long long*>(p);
+    return (int)cudaMemcpyToSymbol(mkq::g_gtrace, &q, sizeof(q));
+}
+#endif

@@ -67,7 +67,15 @@ __global__ void k(int iters, float* out, long long* cyc) {
             } else if (V == 4) {   // 1 x 3-input max (2 new values)
                 x[0] = max3(x[0], x[i], x[i + 1]);
                 x[i] -= 1e-3f;
-            } else {   // 2 x software exp2
+            } else if (V == 6) {   // 2 x I2FP (cvt.rn.f32.s32)
+                x[i] = __int2float_rn(__float_as_int(x[i]) ^ 0x5);
+                x[i + 1] = __int2float_rn(__float_as_int(x[i + 1]) ^ 0x5);
+            } else if (V == 7) {   // 2 x mad.hi.s32 + add.f32x2 (magic int->float)
+                int a0 = __mulhi(__float_as_int(x[i]), 1 << 24) + 0x4B400000;
+                int a1 = __mulhi(__float_as_int(x[i + 1]), 1 << 24) + 0x4B400000;
+                x[i] = __int_as_float(a0) - 12582912.0f;
+                x[i + 1] = __int_as_float(a1) - 12582912.0f;
+            } else if (V == 5) {   // 2 x software exp2
                 x[i] = ex2_poly(x[i]) - 1.0f;
                 x[i + 1] = ex2_poly(x[i + 1]) - 1.0f;
             }
@@ -85,12 +93,12 @@ int main() {
     long long* c;
     cudaMalloc(&o, 1 << 24);
     cudaMalloc(&c, 8);
-    const char* nm[] = {"2x ex2.f32", "1x ex2.f16x2", "1x fma.f32x2", "2x ffma", "1x max3(+1 fadd)", "2x ex2 poly"};
+    const char* nm[] = {"2x ex2.f32", "1x ex2.f16x2", "1x fma.f32x2", "2x ffma", "1x max3(+1 fadd)", "2x ex2 poly", "2x i2fp(+lop)", "2x mulhi+fadd"};
     for (int warps : {8, 16}) {
-        for (int v = 0; v < 6; ++v) {
+        for (int v = 0; v < 8; ++v) {
             const int iters = 2000;
             void (*f)(int, float*, long long*) =
-                v == 0 ? k<0> : v == 1 ? k<1> : v == 2 ? k<2> : v == 3 ? k<3> : v == 4 ? k<4> : k<5>;
+                v == 0 ? k<0> : v == 1 ? k<1> : v == 2 ? k<2> : v == 3 ? k<3> : v == 4 ? k<4> : v == 5 ? k<5> : v == 6 ? k<6> : k<7>;
             f<<<148, 32 * warps>>>(iters, o, c);
             long long h;
             cudaError_t e = cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
