@@ -231,9 +231,10 @@ __device__ unsigned long long* g_gtrace = nullptr;
 constexpr int kGTraceSlots = 512;
 #define GTRACE(tag)                                                                                    \
     do {                                                                                               \
-        if (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && g_gtrace && gt_n < kGTraceSlots) {          \
-            g_gtrace[(threadIdx.x >> 5) * kGTraceSlots * 2 + 2 * gt_n] = (tag);                         \
-            g_gtrace[(threadIdx.x >> 5) * kGTraceSlots * 2 + 2 * gt_n + 1] = clock64();                 \
+        if (blockIdx.x < 2 && (threadIdx.x & 31) == 0 && g_gtrace && gt_n < kGTraceSlots) {           \
+            const int gw = blockIdx.x * 24 + (threadIdx.x >> 5);                                        \
+            g_gtrace[gw * kGTraceSlots * 2 + 2 * gt_n] = (tag);                                          \
+            g_gtrace[gw * kGTraceSlots * 2 + 2 * gt_n + 1] = clock64();                                  \
             ++gt_n;                                                                                    \
         }                                                                                              \
     } while (0)
@@ -241,6 +242,15 @@ constexpr int kGTraceSlots = 512;
 #define GTRACE(tag) \
     do {            \
     } while (0)
+#endif
+
+// Polling policy per wait site.  Sleeping between polls (ptx::mbar_wait_sleep,
+// -DMKQ_EXP_SLEEP) was measured 3% slower on FFN1 than the suspend-hint
+// try_wait loop, so the default polls.
+#ifdef MKQ_EXP_SLEEP
+#define MKQ_WAIT_SLEEP(ns, bar, par) ptx::mbar_wait_sleep<ns>(bar, par)
+#else
+#define MKQ_WAIT_SLEEP(ns, bar, par) ptx::mbar_wait(bar, par)
 #endif
 
 __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
@@ -404,7 +414,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
                 const int m0 = (tile / n_tiles) * 2 * BM + (int)rank * BM;
                 const int n0 = (tile % n_tiles) * BN + (int)rank * BNH;
                 for (int kb = 0; kb < nk; ++kb) {
-                    ptx::mbar_wait(&emptyP[s], ph ^ 1);
+                    MKQ_WAIT_SLEEP(64, &emptyP[s], ph ^ 1);
                     uint8_t* dst = ringP + s * Cfg::kStageP;
                     ptx::mbar_arrive_expect_tx(&fullP[s], Cfg::kStageP);
                     ptx::tma_load_2d(&tmA, &fullP[s], dst, kb * (Cfg::BK / 2), m0);
@@ -427,7 +437,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
                 const int ab = it & 1;
                 const uint32_t aph = (it >> 1) & 1;
                 GTRACE(29);
-                ptx::mbar_wait(&tempty[ab], aph ^ 1);
+                MKQ_WAIT_SLEEP(32, &tempty[ab], aph ^ 1);
                 GTRACE(30);
                 ptx::tc_fence_after();
                 const uint32_t d = tmem_base + ab * BN;
@@ -483,6 +493,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
         if (use_table) L = Lut{th->c0, th->inv_w, th->ncell, ptx::smem_u32(tcells)};
         uint8_t* stage = staging + e * Cfg::kStagePerWarp;
         if (lane == 0) ptx::tma_prefetch_desc(&tmO);
+        // kLut4: (sc, b) of this warp's columns of the NEXT tile, loaded one tile ahead
+        constexpr int kCW = Cfg::kColsPerWarp / 32;
+        float2 v2[kCW];
+        auto load_scales = [&](int tl) {
+#pragma unroll
+            for (int c = 0; c < kCW; ++c) {
+                const int n = (tl % n_tiles) * BN + h * Cfg::kColsPerWarp + 32 * c + lane;
+                float sw = 1.0f, bn = 0.0f;
+                if (tl < num_tiles && n < N) {
+                    sw = __ldg(ep.s_w + n);
+                    bn = ep.bias ? __ldg(ep.bias + n) : 0.0f;
+                }
+                v2[c] = make_float2(sw, bn);
+            }
+        };
+        if constexpr (Cfg::kLut4) load_scales(cluster);
         int it = 0;
         for (int tile = cluster; tile < num_tiles; tile += nclusters, ++it) {
             const int m0 = (tile / n_tiles) * 2 * BM + (int)rank * BM;
@@ -494,19 +520,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
                 // per-warp (sc, b) of this warp's kColsPerWarp columns: no epilogue-wide
                 // barrier per tile, warps slip freely against each other
                 float2* wsb = scb + e * Cfg::kColsPerWarp;
-                const int cw = n0 + h * Cfg::kColsPerWarp;
-                float2 v2[Cfg::kColsPerWarp / 32];
                 bool ok = true;
 #pragma unroll
-                for (int c = 0; c < Cfg::kColsPerWarp / 32; ++c) {
-                    const int n = cw + 32 * c + lane;
-                    float sc = 1.0f, bn = 0.0f;
-                    if (n < N) {
-                        sc = __fmul_rn(ep.s_a, __ldg(ep.s_w + n));
-                        bn = ep.bias ? __ldg(ep.bias + n) : 0.0f;
-                        ok = ok && sc >= 0x1p-118f;
-                    }
-                    v2[c] = make_float2(sc, bn);
+                for (int c = 0; c < kCW; ++c) {
+                    v2[c].x = __fmul_rn(ep.s_a, v2[c].x);   // sc = fl(s_a * s_w[n]) (R4); 1.0 * s_a past N
+                    ok = ok && v2[c].x >= 0x1p-118f;
                 }
                 GTRACE(1);
                 const bool wfold = __all_sync(0xffffffffu, ok);
@@ -520,8 +538,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
                     f[2] = v2[c].y;
                 }
                 __syncwarp();
+                load_scales(tile + nclusters);   // in flight during this tile
                 GTRACE(2);
-                ptx::mbar_wait(&tfull[ab], aph);
+                MKQ_WAIT_SLEEP(128, &tfull[ab], aph);
                 GTRACE(3);
                 ptx::tc_fence_after();
                 const int row0 = m0 + q * 32;
@@ -534,8 +553,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
 #ifdef MKQ_ABL_NOEPI
                     break;
 #endif
-                    if (lane == 0) ptx::tma_store_wait_read<0>();
-                    __syncwarp();
                     GTRACE(4);
                     uint32_t v[32];
                     ptx::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + ab * BN + cl, v);
@@ -548,6 +565,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
                     else
                         epi_lut4<false>(ep, v, sba, tab, a4, b4, use_table, w);
                     GTRACE(6);
+                    // the previous chunk's TMA store must have read the staging block
+                    // (issued a whole chunk of work ago)
+                    if (lane == 0) ptx::tma_store_wait_read<0>();
+                    __syncwarp();
                     *reinterpret_cast<uint4*>(stage + lane * 16) = make_uint4(w[0], w[1], w[2], w[3]);
                     ptx::fence_proxy_async_smem();
                     __syncwarp();
@@ -578,7 +599,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
             const bool fold = !ptx::named_bar_sync_or(1, kEpiThreads, tiny);
             if (et < BN) sb[et] = make_float2(fold ? __fmul_rn(sc, 0x1p-8f) : sc, bn);
             ptx::named_bar_sync(1, kEpiThreads);
-            ptx::mbar_wait(&tfull[ab], aph);
+            MKQ_WAIT_SLEEP(128, &tfull[ab], aph);
             ptx::tc_fence_after();
             const int row0 = m0 + q * 32;
             {
@@ -636,7 +657,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
         for (int tile = cluster; tile < num_tiles; tile += nclusters) {
             for (int kb = 0; kb < nk; ++kb) {
                 GTRACE(19);
-                ptx::mbar_wait(&fullP[sp], php);
+                MKQ_WAIT_SLEEP(32, &fullP[sp], php);
                 GTRACE(20);
                 const uint32_t src = ringP_s + (uint32_t)sp * Cfg::kStageP + src_off;
                 uint4 pk[kPer];
@@ -644,7 +665,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
 #pragma unroll
                 for (int i = 0; i < kPer; ++i) pk[i] = ptx::lds128(src + (uint32_t)i * (kRowsPerPass * 64u));
 #endif
-                ptx::mbar_wait(&empty8[s8], ph8 ^ 1);
+                MKQ_WAIT_SLEEP(32, &empty8[s8], ph8 ^ 1);
                 GTRACE(21);
                 const uint32_t dst = ring8_s + (uint32_t)s8 * Cfg::kStage8;
 #ifndef MKQ_DBG_NO_UNPACK

@@ -68,6 +68,26 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     }
 }
 
+// Wait with an explicit sleep between polls, for roles that wait long and are
+// not on the critical path: the suspend-hint form above wakes on every
+// barrier event of the CTA, and in a kernel with a dozen busy barriers the
+// waiting warps then spin through issue slots the working warps need.
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.b32 %0, 1, 0, P1;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+template <int kNs>
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+    while (!mbar_test(bar, parity)) __nanosleep(kNs);
+}
+
 // ------------------------------------------------------------------ fences
 // Generic-proxy writes to shared memory -> visible to the async proxy
 // (tensor core / TMA reads).  Executed by every writing thread.
