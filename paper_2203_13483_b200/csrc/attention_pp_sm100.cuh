@@ -41,6 +41,13 @@ using attn2::mma_f16_ss_warp;
 using attn2::mma_f16_ts_warp;
 using attn2::Params;
 using attn2::tmem_st_x16;
+using attn2::ffma2;
+using attn2::fadd2;
+using attn2::ex2_fma2;
+#ifndef MKQ_ATTN_POLY_FROM
+#define MKQ_ATTN_POLY_FROM 6   // pairs (i & 7) >= this use the FMA-pipe exp2 (tools/attn_poly.sh: 8 537 us, 6 523, 5 549, 4 561)
+#endif
+constexpr int kPolyFrom = MKQ_ATTN_POLY_FROM;
 
 constexpr int kBQ = 128, kBK = 128, kD = 64;
 constexpr int kStages = 3;
@@ -310,7 +317,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
                 TRACE(4);
                 const float nmx = -m;
-                float ps[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+                float2 ps2[2] = {make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f)};
                 if (nb > 0) {   // P_x is free once PV_x of the previous block completed
                     ptx::mbar_wait(&pv_done[x], (nb - 1) & 1);
                     ptx::tc_fence_after();
@@ -321,15 +328,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                     uint32_t pk[16];
 #pragma unroll
                     for (int i = 0; i < 16; ++i) {
+                        const float2 x2 = ffma2(make_float2(__uint_as_float(sv[cc][2 * i]), __uint_as_float(sv[cc][2 * i + 1])),
+                                                make_float2(c, c), make_float2(nmx, nmx));
 #ifdef MKQ_ABL_NOEXP   // ablation (diagnostics only): no MUFU
-                        const float e0 = fmaf(__uint_as_float(sv[cc][2 * i]), c, nmx);
-                        const float e1 = fmaf(__uint_as_float(sv[cc][2 * i + 1]), c, nmx);
+                        const float2 e2 = x2;
 #else
-                        const float e0 = ex2f(fmaf(__uint_as_float(sv[cc][2 * i]), c, nmx));
-                        const float e1 = ex2f(fmaf(__uint_as_float(sv[cc][2 * i + 1]), c, nmx));
+                        // 2 of every 8 pairs on the FMA pipe (ex2_fma2), the rest on
+                        // MUFU: balances the two pipes (XU 8 cycles / FMA ~6 per element)
+                        const float2 e2 = (i & 7) >= kPolyFrom ? ex2_fma2(x2) : make_float2(ex2f(x2.x), ex2f(x2.y));
 #endif
-                        ps[i & 3] += e0 + e1;
-                        pk[i] = h2(e0, e1);
+                        ps2[i & 1] = fadd2(ps2[i & 1], e2);
+                        pk[i] = h2(e2.x, e2.y);
                     }
 #ifdef MKQ_ABL_NOST
                     if (pk[0] == 0x12345678u && pk[15] == 0x9abcdef0u)
@@ -342,7 +351,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (x == 1 && j + 1 < I.nblk) ptx::named_bar_arrive(5 + q, 64);
                 }
 #endif
-                l += (ps[0] + ps[1]) + (ps[2] + ps[3]);
+                l += (ps2[0].x + ps2[1].x) + (ps2[0].y + ps2[1].y);
                 TRACE(14);
                 ptx::tmem_st_wait();
                 ptx::tc_fence_before();

@@ -144,6 +144,33 @@ __device__ __forceinline__ float ex2_fma(float x) {
     return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
 
+// packed fp32 pairs (sm_100 f32x2: one instruction, two IEEE RN results)
+__device__ __forceinline__ uint64_t f2u(float2 a) { return *reinterpret_cast<const uint64_t*>(&a); }
+__device__ __forceinline__ float2 u2f(uint64_t a) { return *reinterpret_cast<const float2*>(&a); }
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+    uint64_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b)), "l"(f2u(c)));
+    return u2f(r);
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+    uint64_t r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b)));
+    return u2f(r);
+}
+// ex2_fma on a pair, in f32x2 arithmetic (6 pair-ops + 2 clamps + 2 IMAD)
+__device__ __forceinline__ float2 ex2_fma2(float2 x) {
+    x.x = fmaxf(x.x, -125.0f);
+    x.y = fmaxf(x.y, -125.0f);
+    const float2 t = fadd2(x, make_float2(12582912.0f, 12582912.0f));
+    const float2 n = fadd2(t, make_float2(-12582912.0f, -12582912.0f));
+    const float2 f = ffma2(n, make_float2(-1.0f, -1.0f), x);
+    float2 p = ffma2(make_float2(0x1.ca1d02p-5f, 0x1.ca1d02p-5f), f, make_float2(0x1.f0ed48p-3f, 0x1.f0ed48p-3f));
+    p = ffma2(p, f, make_float2(0x1.62e0c2p-1f, 0x1.62e0c2p-1f));
+    p = ffma2(p, f, make_float2(0x1.fff61ap-1f, 0x1.fff61ap-1f));
+    return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                       __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
+
 __device__ __forceinline__ uint32_t h2(float a, float b) {
     __half2 v = __floats2half2_rn(a, b);
     return *reinterpret_cast<uint32_t*>(&v);
