@@ -62,6 +62,13 @@ struct Gemm2Cfg {
     static constexpr int kStagePerWarp = kLut4 ? 512 : 2048;   // 32 rows x 16 B (int4) / 64 B output block per warp
     static constexpr int kStaging = kEpiWarps * kStagePerWarp;
     static constexpr int kTabBytes = kLut4 ? (int)rq::kSmem4Bytes : (int)rq::kSmemBytes;
+    // kLut4 register split (setmaxnreg; must fit the launch allocation)
+    static constexpr int kRegLaunch = ((65536 / kThreads) & ~7) > 255 ? 248 : ((65536 / kThreads) & ~7);
+    static constexpr int kRegProd = 40;
+    static constexpr int kRegUnp = kUnpWarps >= 8 ? 48 : 56;
+    static constexpr int kRegEpi =
+        ((kRegLaunch * kThreads - 128 * kRegProd - 32 * kUnpWarps * kRegUnp) / (32 * kEpiWarps)) & ~7;
+    static_assert(!kLut4 || (kRegEpi >= kRegLaunch && kRegEpi <= 256), "register split");
     static_assert(kColsPerWarp % 32 == 0, "epilogue column split");
     static constexpr int kBarBytes = 8 * (2 * S8 + 2 * SP + 4) + 16;
     static constexpr int kSmem = 1024 + S8 * kStage8 + SP * kStageP + kTabBytes + kScb + kStaging + kBarBytes;
@@ -401,10 +408,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     // kLut4: register reallocation per warpgroup (each executes one setmaxnreg
-    // at one PC): producer/MMA group 40, unpack 56, epilogue (the latency-bound
-    // role) the rest of the launch allocation (80 x 768), 96
+    // at one PC): producer/MMA group kRegProd, unpack kRegUnp, epilogue (the
+    // latency-bound role) the rest of the launch allocation, kRegEpi
     if (warp < 4) {
-    if constexpr (Cfg::kLut4) asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
+    if constexpr (Cfg::kLut4) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(Cfg::kRegProd));
     if (warp == 0) {
         // ---------------------------------------------------- TMA producer (both CTAs)
         if (lane == 0) {
@@ -460,7 +467,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
         }
     }
     } else if (warp < 4 + Cfg::kEpiWarps) {
-        if constexpr (Cfg::kLut4) asm volatile("setmaxnreg.inc.sync.aligned.u32 96;");
+        if constexpr (Cfg::kLut4) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(Cfg::kRegEpi));
         // ---------------------------------------------------- epilogue (both CTAs)
         const int e = warp - 4;           // 0..7
         const int q = warp & 3;           // TMEM lane quadrant (warp % 4)
@@ -638,7 +645,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
         }
         if (lane == 0) ptx::tma_store_wait<0>();
     } else {
-        if constexpr (Cfg::kLut4) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+        if constexpr (Cfg::kLut4) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(Cfg::kRegUnp));
         // ---------------------------------------------------- int4 -> int8 unpack (both CTAs)
         const int u = threadIdx.x - 32 * (4 + Cfg::kEpiWarps);
         constexpr int kChunks = (BM + BNH) * (Cfg::BK / 32);   // 16-byte packed chunks per stage
