@@ -71,6 +71,7 @@ def lib():
         L.oracle_scale_grad_ste.restype = ctypes.c_double
         L.oracle_scale_grad_mse.argtypes = [P, I64, F, I, I]
         L.oracle_scale_grad_mse.restype = ctypes.c_double
+        L.oracle_ste_grad_x.argtypes = [P, P, I64, F, I, I, P]
         _lib = L
     return _lib
 
@@ -214,7 +215,8 @@ def absmax_scale(w, l_max, per_row=True) -> np.ndarray:
 
 
 def scale_grad_ste(x, s, qmin=-8, qmax=7) -> float:
-    """§4.1.1: sum_i(-x_i/s + round(x_i/s))."""
+    """§4.1.1: sum_i(-x_i/s + round(x_i/s)); clipped elements
+    contribute their clamped code (LSQ, reading R17)."""
     x = np.ascontiguousarray(x, dtype=np.float32).ravel()
     return lib().oracle_scale_grad_ste(_p(x), x.size, float(np.float32(s)), qmin, qmax)
 
@@ -223,6 +225,17 @@ def scale_grad_mse(x, s, qmin=-8, qmax=7) -> float:
     """§4.1.2: 2 sum_i (Q[x_i]-x_i) round(x_i/s)."""
     x = np.ascontiguousarray(x, dtype=np.float32).ravel()
     return lib().oracle_scale_grad_mse(_p(x), x.size, float(np.float32(s)), qmin, qmax)
+
+
+def ste_grad_x(x, grad_y, s, qmin=-8, qmax=7) -> np.ndarray:
+    """STE input gradient: grad_y where x is not clipped, else 0 (R18)."""
+    x = np.ascontiguousarray(x, dtype=np.float32).ravel()
+    gy = np.ascontiguousarray(grad_y, dtype=np.float32).ravel()
+    assert gy.size == x.size
+    out = np.empty_like(x)
+    _chk(lib().oracle_ste_grad_x(_p(x), _p(gy), x.size, float(np.float32(s)), qmin, qmax, _p(out)),
+         "ste_grad_x")
+    return out
 
 
 def abs_quantile(x, p=0.9999) -> np.float32:

@@ -295,18 +295,36 @@ int oracle_absmax_scale(const float *w, int64_t rows, int64_t cols, int64_t ld,
     return OK;
 }
 
-/* QAT-side scale gradients of §4.1 (NEXT(3) in SURVEY §8f):               */
-/* STE: sum_i (-x_i/s + round(x_i/s))                          */
-/* MSE: 2 * sum_i (Q[x_i] - x_i) * round(x_i/s)                */
-/* round(.) is the clamped code (Eq.1), reading R1/R2.  Summed in double.  */
+/* QAT-side gradients of §4.1 (NEXT(3) in SURVEY §8f).                     */
+/* "Clipped" = the unclamped code rint(x/s) lies outside [qmin, qmax]      */
+/* (reading R18).                                                          */
+static int clipped1(float x, float s, int qmin, int qmax)
+{
+    float r = nearbyintf(x / s);
+    return r < (float)qmin || r > (float)qmax;
+}
+
+/* STE scale gradient: sum_i (-x_i/s + round(x_i/s)), the     */
+/* derivation of "previous work" [kdlsq, esser2019learned].  The   */
+/* paper's derivation ignores the clamp; for a clipped x_i, Q[x_i] =       */
+/* s*qmax (or s*qmin), whose derivative is the clamped code itself (LSQ's  */
+/* rule) -- reading R17.  Summed in double.                                */
 double oracle_scale_grad_ste(const float *x, int64_t n, float s, int qmin, int qmax)
 {
     double g = 0.0;
-    for (int64_t i = 0; i < n; ++i)
-        g += -(double)x[i] / (double)s + (double)quant1(x[i], s, qmin, qmax);
+    for (int64_t i = 0; i < n; ++i) {
+        int q = quant1(x[i], s, qmin, qmax);
+        if (clipped1(x[i], s, qmin, qmax))
+            g += (double)q;
+        else
+            g += -(double)x[i] / (double)s + (double)q;
+    }
     return g;
 }
 
+/* MSE scale gradient: 2 * sum_i (Q[x_i] - x_i) * round(x_i/s) */
+/* with round(.) the clamped code (Eq.1): Q_{s+ds}[x] = (s+ds) q holds for */
+/* clipped elements too.  Summed in double.                                */
 double oracle_scale_grad_mse(const float *x, int64_t n, float s, int qmin, int qmax)
 {
     double g = 0.0;
@@ -316,4 +334,15 @@ double oracle_scale_grad_mse(const float *x, int64_t n, float s, int qmin, int q
         g += (Q - (double)x[i]) * (double)q;
     }
     return 2.0 * g;
+}
+
+/* STE input gradient ("d round / d . = 1"): dL/dx_i = dL/dQ_i where */
+/* x_i is not clipped, 0 where it is (reading R18; LSQ / PyTorch           */
+/* fake-quant convention -- the paper is silent on the clamp).             */
+int oracle_ste_grad_x(const float *x, const float *grad_y, int64_t n, float s,
+                      int qmin, int qmax, float *grad_x)
+{
+    for (int64_t i = 0; i < n; ++i)
+        grad_x[i] = clipped1(x[i], s, qmin, qmax) ? 0.0f : grad_y[i];
+    return OK;
 }

@@ -44,6 +44,44 @@ def test_paper_scale_gradients_P151_P187():
     assert mse(0.9) < mse(1.0)
 
 
+def test_qat_gradients_hand_worked_with_clipping():
+    """x=(0.2,0.9,-0.3,7.6,-9.0), s=1, codes [-8,7] (worked by hand):
+    unclamped codes (0,1,0,8,-9) -> the last two are clipped (R18).
+    STE (P:138-142 + LSQ rule for clipped, R17): (-0.2+0)+(-0.9+1)+(0.3+0)+7-8 = -0.8.
+    MSE (P:181): 2[(0-.2)0 + (1-.9)1 + (0+.3)0 + (7-7.6)7 + (-8+9)(-8)] = -24.2.
+    STE input gradient: grad_y passes where not clipped -> (1,2,3,0,0)."""
+    x = np.array([0.2, 0.9, -0.3, 7.6, -9.0], np.float32)
+    assert oracle.scale_grad_ste(x, 1.0) == pytest.approx(-0.8, abs=1e-6)
+    assert oracle.scale_grad_mse(x, 1.0) == pytest.approx(-24.2, abs=1e-5)
+    gx = oracle.ste_grad_x(x, np.array([1, 2, 3, 4, 5], np.float32), 1.0)
+    assert gx.tolist() == [1.0, 2.0, 3.0, 0.0, 0.0]
+    # a code that rounds onto the bound is not clipped: 7.4 -> 7, -8.4 -> -8
+    y = np.array([7.4, -8.4], np.float32)
+    assert oracle.ste_grad_x(y, np.ones(2, np.float32), 1.0).tolist() == [1.0, 1.0]
+
+
+def test_qat_gradients_match_torch_lsq():
+    """Library pin: PyTorch's LSQ fake-quant (esser2019learned, the 'previous
+    work' of P:128) with grad_factor 1 and dL/dQ = 1 gives d/ds = the STE
+    scale gradient and d/dx = the STE input mask.  Inputs are kept away from
+    rounding boundaries, where torch's x*(1/s) and Eq.1's x/s (R3) agree."""
+    import torch
+    rng = np.random.default_rng(21)
+    s = np.float32(0.37)
+    x = (rng.standard_normal(20000) * 1.5).astype(np.float32)
+    v = x.astype(np.float64) / np.float64(s)
+    x = x[np.abs(np.abs(v - np.floor(v)) - 0.5) > 1e-3]
+    xt = torch.from_numpy(x.copy()).requires_grad_(True)
+    st = torch.tensor([float(s)], requires_grad=True)
+    y = torch._fake_quantize_learnable_per_tensor_affine(xt, st, torch.tensor([0.0]), -8, 7, 1.0)
+    y.backward(torch.ones_like(y))
+    assert np.array_equal(y.detach().numpy(), oracle.fake_quant(x, s, -8, 7))
+    assert np.array_equal(xt.grad.numpy(), oracle.ste_grad_x(x, np.ones_like(x), s))
+    assert (~(xt.grad.numpy() > 0)).sum() > 10          # some clipped elements exercised
+    g = oracle.scale_grad_ste(x, s)
+    assert float(st.grad) == pytest.approx(g, rel=1e-4, abs=1e-2)
+
+
 def test_mse_gradient_matches_finite_difference():
     """§4.1.2: away from rounding ties the MSE gradient is the
     derivative of sum (Q[x]-x)^2 w.r.t. s (codes fixed under a small ds)."""
@@ -286,9 +324,16 @@ def test_activation_quantile_half_normal():
     q = oracle.abs_quantile(x, 0.9999)
     assert abs(q - 3.8906) < 0.06       # half-normal 0.9999 quantile
     assert oracle.abs_quantile(np.ones(100), 0.9999) == 1.0
-    u = np.random.default_rng(11).random(10_000)
-    assert oracle.abs_quantile(u) == pytest.approx(np.sort(u)[-1] * 0.9999 + np.sort(u)[-2] * 0.0001, rel=1e-6) \
-        or abs(oracle.abs_quantile(u) - 0.9999) < 1e-3
+    # hand cases: |x| sorted = (1,2,3,4); p=0.5 -> pos 1.5 -> 2.5; p=0 -> min, p=1 -> max
+    t = np.array([3, -1, 2, -4], np.float32)
+    assert oracle.abs_quantile(t, 0.5) == np.float32(2.5)
+    assert oracle.abs_quantile(t, 0.0) == np.float32(1.0)
+    assert oracle.abs_quantile(t, 1.0) == np.float32(4.0)
+    # library pin: numpy's linear-interpolation quantile (same definition)
+    u = np.random.default_rng(11).standard_normal(100_003).astype(np.float32)
+    for p in (0.9999, 0.5, 0.123456):
+        ref = np.quantile(np.abs(u.astype(np.float64)), p, method="linear")
+        assert oracle.abs_quantile(u, p) == pytest.approx(ref, rel=2e-7)
 
 
 def test_bit_accounting_P30():
