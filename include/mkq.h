@@ -198,6 +198,44 @@ MKQ_API mkq_status mkq_interleave_blocks(const void *src, void *dst, int64_t g, 
                                          int64_t ld_dst_bytes, void *stream);
 
 /* ------------------------------------------------------------------------
+ * QAT-side fake quantization with the §4.1 scale
+ * gradients, one HBM pass over a contiguous fp32 tensor x [n]:
+ *   q_i   = clamp(rint_even(x_i / s), qmin, qmax)       Eq.1, R1-R3
+ *   y_i   = fl32(s * q_i)                                fake-quant Q[x]
+ *   clip_i: rint_even(x_i / s) lies outside [qmin, qmax]  (R18)
+ *   grad_x_i = clip_i ? 0 : grad_y_i                     STE input gradient (R18)
+ *   grad_s[0] = sum_i (clip_i ? q_i : q_i - x_i / s)     STE scale gradient (
+ *                                                         LSQ rule for clipped x_i, R17)
+ *   grad_s[1] = 2 sum_i (s q_i - x_i) q_i                MSE scale gradient
+ * scale  [device] fp32, 1 value (> 0, finite; not inspected on the host).
+ * y, grad_x [device] fp32 [n] or NULL (not computed); grad_y [device] fp32 [n],
+ *        required with grad_x.  grad_s [device] fp64 [2] or NULL.
+ * ws     [device] >= mkq_fake_quant_workspace_size(n) bytes, 16-byte aligned
+ *        (per-block partial sums; the final fold is in a fixed order, so
+ *        grad_s is deterministic).  The fp64 sums equal the oracle's up to
+ *        summation order; y and grad_x are bit-exact.
+ * qmin < qmax within [-128, 127] (any bit width <= 8).  n == 0: grad_s = 0.
+ * ---------------------------------------------------------------------- */
+MKQ_API size_t mkq_fake_quant_workspace_size(int64_t n);
+MKQ_API mkq_status mkq_fake_quant(const float *x, int64_t n, const float *scale, int qmin, int qmax,
+                                  float *y, const float *grad_y, float *grad_x, double *grad_s,
+                                  void *ws, size_t ws_bytes, void *stream);
+
+/* activation-scale calibration on the GPU, P:72 ("top
+ * 0.01% largest value ... as the initial scale", normalised by l_max, R6):
+ *   a = |x| sorted ascending; pos = p (n-1); lo = floor(pos);
+ *   hi = min(lo+1, n-1); quant = fl32(a[lo] + (pos-lo)(a[hi]-a[lo])) (fp64);
+ *   *s_out = fl32(quant / l_max).
+ * The order statistics are exact (radix select on the bit patterns of |x|,
+ * no sort, no host copy); bit-identical to the definition.
+ * x [device] fp32 [n], n >= 1, finite.  p in [0, 1] (0.9999 in the paper).
+ * s_out [device] fp32 [1].  ws [device] >= mkq_act_scale_workspace_size()
+ * bytes, 16-byte aligned. */
+MKQ_API size_t mkq_act_scale_workspace_size(void);
+MKQ_API mkq_status mkq_act_scale(const float *x, int64_t n, double p, float l_max, float *s_out,
+                                 void *ws, size_t ws_bytes, void *stream);
+
+/* ------------------------------------------------------------------------
  * One quantized post-LN BERT encoder layer (§8a rows a1-a8 composed):
  *   c   = Q(h; s_qkv_in)                                   a1
  *   qkv = f16( Linear_{W^{QKV}}(c) )                        a2-a4

@@ -35,6 +35,10 @@ SIGNATURES = {
     "mkq_attention": (I32, [P, I64, I64, I64, P, I64, I32, I32, I32, F32, I32, I32, P, I64, P]),
     "mkq_residual_layernorm": (I32, [P, P, I64, I64, I64, P, P, F32, P, I32, F32, I32, I32, P, I64, P]),
     "mkq_interleave_blocks": (I32, [P, P, I64, I64, I64, I64, P]),
+    "mkq_fake_quant_workspace_size": (SZ, [I64]),
+    "mkq_fake_quant": (I32, [P, I64, P, I32, I32, P, P, P, P, P, SZ, P]),
+    "mkq_act_scale_workspace_size": (SZ, []),
+    "mkq_act_scale": (I32, [P, I64, ctypes.c_double, F32, P, P, SZ, P]),
     "mkq_bert_layer_workspace_size": (SZ, [P, I64]),
     "mkq_bert_layer": (I32, [P, P, I64, I64, P, I64, P, P, SZ, P]),
 }

@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
+#include <algorithm>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -22,6 +23,8 @@
 #include "requant.cuh"
 #include "layernorm.cuh"
 #include "quantize.cuh"
+#include "qat.cuh"
+#include "calib.cuh"
 
 #define MKQ_VERSION 10000
 
@@ -657,6 +660,83 @@ mkq_status mkq_interleave_blocks(const void* src, void* dst, int64_t g, int64_t 
         static_cast<const uint8_t*>(src), static_cast<uint8_t*>(dst), g, rows, cb, ldd);
     cudaError_t e = cudaPeekAtLastError();
     return e == cudaSuccess ? MKQ_OK : cuda_fail(e, "interleave launch");
+}
+
+// ------------------------------------------------------------------ QAT / calibration
+static constexpr int kQatMaxBlocks = 2048;
+
+size_t mkq_fake_quant_workspace_size(int64_t) { return kQatMaxBlocks * sizeof(mkq::qat::Partial); }
+
+mkq_status mkq_fake_quant(const float* x, int64_t n, const float* scale, int qmin, int qmax, float* y,
+                          const float* grad_y, float* grad_x, double* grad_s, void* ws, size_t ws_bytes,
+                          void* stream) {
+    if (n < 0) return fail(MKQ_ERR_SHAPE, "negative n");
+    if (!scale || (n > 0 && !x)) return fail(MKQ_ERR_NULL, "x and scale are required");
+    if (grad_x && !grad_y) return fail(MKQ_ERR_NULL, "grad_x needs grad_y");
+    if (!ws) return fail(MKQ_ERR_NULL, "a workspace is required");
+    if (n > (int64_t(1) << 40)) return fail(MKQ_ERR_SHAPE, "n too large");
+    if (ws_bytes < mkq_fake_quant_workspace_size(n))
+        return fail(MKQ_ERR_WORKSPACE, "workspace needs %zu bytes", mkq_fake_quant_workspace_size(n));
+    if ((reinterpret_cast<uintptr_t>(grad_s) & 7) || (ws && (reinterpret_cast<uintptr_t>(ws) & 15)))
+        return fail(MKQ_ERR_ALIGN, "grad_s 8-byte, ws 16-byte aligned");
+    if (!code_range_ok(8, qmin, qmax)) return fail(MKQ_ERR_RANGE, "need -128 <= qmin < qmax <= 127");
+    int sms = 0;
+    mkq_status s = check_device(&sms);
+    if (s != MKQ_OK) return s;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int vec = aligned16(x) && (!y || aligned16(y)) && (!grad_y || aligned16(grad_y)) &&
+                    (!grad_x || aligned16(grad_x));
+    int64_t blocks = ((n + 3) / 4 + mkq::qat::kThreads - 1) / mkq::qat::kThreads;
+    const int64_t cap = std::min<int64_t>(kQatMaxBlocks, (int64_t)sms * 8);
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    if (!y && !grad_x && !grad_s) return MKQ_OK;
+    auto* part = static_cast<mkq::qat::Partial*>(ws);
+    mkq::qat::fake_quant_grad_kernel<<<(int)blocks, mkq::qat::kThreads, 0, st>>>(
+        x, n, scale, qmin, qmax, y, grad_y, grad_x, part, vec);
+    if (grad_s)
+        mkq::qat::fake_quant_finalize_kernel<<<1, mkq::qat::kThreads, 0, st>>>(part, (int)blocks, scale, grad_s);
+    cudaError_t e = cudaPeekAtLastError();
+    return e == cudaSuccess ? MKQ_OK : cuda_fail(e, "fake_quant launch");
+}
+
+size_t mkq_act_scale_workspace_size(void) { return mkq::calib::kWsBytes; }
+
+mkq_status mkq_act_scale(const float* x, int64_t n, double p, float l_max, float* s_out, void* ws, size_t ws_bytes,
+                         void* stream) {
+    if (n < 0) return fail(MKQ_ERR_SHAPE, "negative n");
+    if (!x || !s_out || !ws) return fail(MKQ_ERR_NULL, "x, s_out and ws are required");
+    if (n == 0) return fail(MKQ_ERR_SHAPE, "empty input has no quantile");
+    if (ws_bytes < mkq::calib::kWsBytes) return fail(MKQ_ERR_WORKSPACE, "workspace needs %zu bytes", mkq::calib::kWsBytes);
+    if (reinterpret_cast<uintptr_t>(ws) & 15) return fail(MKQ_ERR_ALIGN, "ws must be 16-byte aligned");
+    if (!(p >= 0.0 && p <= 1.0)) return fail(MKQ_ERR_RANGE, "p must be in [0, 1]");
+    if (!finite_pos(l_max)) return fail(MKQ_ERR_SCALE, "l_max must be > 0 and finite");
+    int sms = 0;
+    mkq_status s = check_device(&sms);
+    if (s != MKQ_OK) return s;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    // index arithmetic of the definition (R6): pos = p (n-1), fp64
+    const double pos = p * (double)(n - 1);
+    const double flo = std::floor(pos);
+    const unsigned long long lo = (unsigned long long)flo;
+    const unsigned long long hi = std::min<unsigned long long>(lo + 1, (unsigned long long)(n - 1));
+    const double frac = pos - flo;
+    using namespace mkq::calib;
+    auto* state = static_cast<State*>(ws);
+    auto* hist = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + 64);
+    const int vec = aligned16(x);
+    int64_t blocks = (n / (vec ? 4 : 1) + kThreads - 1) / kThreads;
+    blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)sms * 2));
+    init_kernel<<<1, kThreads, 0, st>>>(state, hist, lo, hi);
+    hist_kernel<0><<<(int)blocks, kThreads, 0, st>>>(x, n, vec, state, hist);
+    select_kernel<0><<<1, kThreads, 0, st>>>(state, hist);
+    hist_kernel<1><<<(int)blocks, kThreads, 0, st>>>(x, n, vec, state, hist);
+    select_kernel<1><<<1, kThreads, 0, st>>>(state, hist);
+    hist_kernel<2><<<(int)blocks, kThreads, 0, st>>>(x, n, vec, state, hist);
+    select_kernel<2><<<1, kThreads, 0, st>>>(state, hist);
+    finalize_kernel<<<1, 1, 0, st>>>(state, frac, l_max, s_out);
+    cudaError_t e = cudaPeekAtLastError();
+    return e == cudaSuccess ? MKQ_OK : cuda_fail(e, "act_scale launch");
 }
 
 // ------------------------------------------------------------------ BERT layer

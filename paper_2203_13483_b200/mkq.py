@@ -14,7 +14,8 @@ from ._lib import (OUT_BF16, OUT_F16, OUT_F32, OUT_I32, OUT_I4, OUT_I8, MkqEpilo
                    check, lib)
 
 __all__ = ["mkq_requant_table", "mkq_quantize_pack", "mkq_absmax_scale", "mkq_gemm_w4a4", "mkq_gemm_w8a8",
-           "mkq_attention", "mkq_residual_layernorm", "mkq_bert_layer", "mkq_interleave_blocks", "out_dtype_bytes",
+           "mkq_attention", "mkq_residual_layernorm", "mkq_bert_layer", "mkq_interleave_blocks", "mkq_fake_quant",
+           "mkq_act_scale", "out_dtype_bytes",
            "OUT_F32", "OUT_BF16", "OUT_I32", "OUT_I4", "OUT_I8", "OUT_F16"]
 
 
@@ -63,6 +64,41 @@ def mkq_absmax_scale(x: torch.Tensor, l_max: float, per_row: bool = True, out: O
         out = torch.empty(rows if per_row else 1, dtype=torch.float32, device=x.device)
     check("mkq_absmax_scale", lib().mkq_absmax_scale(_ptr(x), rows, cols, x.stride(0), int(per_row),
                                                      float(l_max), _ptr(out), _stream(stream)))
+    return out
+
+
+def mkq_fake_quant(x: torch.Tensor, scale: torch.Tensor, qmin: int = -8, qmax: int = 7, grad_y=None,
+                   want_y: bool = True, want_grad_s: bool = True, ws: Optional[torch.Tensor] = None, stream=None):
+    """§4.1 QAT step: fake-quant y = s*q, STE input gradient
+    (given grad_y) and the STE / MSE scale gradients, one HBM pass.
+    Returns (y | None, grad_x | None, grad_s fp64 [2] = {STE, MSE} | None)."""
+    assert x.is_contiguous() and x.dtype == torch.float32
+    n = x.numel()
+    y = torch.empty_like(x) if want_y else None
+    gx = torch.empty_like(x) if grad_y is not None else None
+    if grad_y is not None:
+        assert grad_y.is_contiguous() and grad_y.shape == x.shape
+    gs = torch.empty(2, dtype=torch.float64, device=x.device) if want_grad_s else None
+    nb = int(lib().mkq_fake_quant_workspace_size(n))
+    if ws is None or ws.numel() < nb:
+        ws = torch.empty(nb, dtype=torch.uint8, device=x.device)
+    check("mkq_fake_quant", lib().mkq_fake_quant(_ptr(x), n, _ptr(scale), qmin, qmax, _ptr(y), _ptr(grad_y),
+                                                 _ptr(gx), _ptr(gs), _ptr(ws), ws.numel(), _stream(stream)))
+    return y, gx, gs
+
+
+def mkq_act_scale(x: torch.Tensor, l_max: float = 7.0, p: float = 0.9999, out: Optional[torch.Tensor] = None,
+                  ws: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """P:72 calibration on the GPU: fl32(quantile_p(|x|)) / l_max (R6), an
+    exact radix select (fp32 device tensor [1])."""
+    assert x.is_contiguous() and x.dtype == torch.float32
+    if out is None:
+        out = torch.empty(1, dtype=torch.float32, device=x.device)
+    nb = int(lib().mkq_act_scale_workspace_size())
+    if ws is None or ws.numel() < nb:
+        ws = torch.empty(nb, dtype=torch.uint8, device=x.device)
+    check("mkq_act_scale", lib().mkq_act_scale(_ptr(x), x.numel(), float(p), float(l_max), _ptr(out), _ptr(ws),
+                                               ws.numel(), _stream(stream)))
     return out
 
 

@@ -1,9 +1,8 @@
 """Layer assembly on top of the C ABI: offline weight prep (§8a-a0), offline
 activation-scale calibration (★s host rule) and the
 mixed-precision stack (P:243 'start from the last layer'; P:46 50% int4 +
-50% int8).  Marshalling only: all arithmetic runs in libmkq.so kernels, except
-the calibration statistic (the 99.99th percentile of |activation|, a host
-rule of the offline calibration step)."""
+50% int8).  Marshalling only: all arithmetic runs in libmkq.so kernels,
+including the calibration statistic (mkq_act_scale)."""
 from __future__ import annotations
 
 from typing import Dict, List, Optional, Sequence
@@ -30,18 +29,11 @@ def prepare_weight(w: torch.Tensor, bits: int):
     return q, s_w
 
 
-def abs_quantile(x: torch.Tensor, p: float = 0.9999) -> np.float32:
-    """Calibration statistic (P:72 'top 0.01% largest value'): sort-based
-    p-quantile of |x| with linear interpolation, fp64, rounded to fp32."""
-    a = np.sort(np.abs(x.detach().double().cpu().numpy()).ravel())
-    pos = p * (a.size - 1)
-    lo = int(np.floor(pos))
-    hi = min(lo + 1, a.size - 1)
-    return np.float32(a[lo] + (pos - lo) * (a[hi] - a[lo]))
-
-
-def act_scale(x: torch.Tensor, l_max: int) -> float:
-    return float(np.float32(abs_quantile(x)) / np.float32(l_max))
+def act_scale(x: torch.Tensor, l_max: int, p: float = 0.9999) -> float:
+    """s_a = fl32(quantile_p(|x|)) / l_max (P:72 'top 0.01%', R6), computed
+    on the GPU by mkq_act_scale (exact radix select); one scalar read back,
+    because mkq_layer carries the static scales as host floats."""
+    return float(M.mkq_act_scale(x.contiguous(), float(l_max), p).item())
 
 
 def build_layer(params, bits: int, device="cuda", scales: Optional[Dict[str, float]] = None,
