@@ -160,7 +160,16 @@ MKQ_API mkq_status mkq_gemm_w8a8(const void *a, int64_t lda_bytes, const void *w
                          const float *bias, const mkq_epilogue *epi, void *out,
                          int64_t ldo_bytes, void *ws, size_t ws_bytes, void *stream);
 
+/* Workspace of mkq_gemm_w4a4 / mkq_gemm_w8a8 for an (M, N, K) call: 0 (no
+ * workspace is needed).  For small M (the paper's Table
+ * 2 regime) the library splits K over the CTAs of a thread-block cluster and
+ * sums the exact int32 partials (R15) through distributed shared memory. */
 MKQ_API size_t mkq_gemm_workspace_size(int64_t M, int64_t N, int64_t K);
+
+/* Diagnostics / tests: GEMM tile plan for small M.  -1 = heuristic (default;
+ * also the MKQ_SMALL_M environment variable), 0 = never the small-M plan,
+ * 1 = always.  Results are identical in every mode. */
+MKQ_API void mkq_set_small_m_mode(int mode);
 
 /* ------------------------------------------------------------------------
  * §8a-a8 glue (★s): multi-head self-attention core, Eq.3-5 (with

@@ -67,6 +67,7 @@ struct GemmCfg {
     static constexpr int kStageP = kAP + kBP;
     static constexpr int S8 = kInt4 ? (BN == 256 ? 3 : 4) : 4;
     static constexpr int SP = kInt4 ? (BN == 256 ? 3 : 4) : 0;
+    static_assert(BN == 64 || BN == 128 || BN == 256, "BN");
     static constexpr int kThreads = kInt4 ? 384 : 256;
     static constexpr uint32_t kTmemCols = 2 * BN;   // double-buffered accumulator
     static constexpr int kBarBytes = 8 * (2 * S8 + 2 * SP + 4) + 16;
@@ -75,27 +76,8 @@ struct GemmCfg {
 };
 
 // ------------------------------------------------------------------ epilogue store
-template <bool kInt4>
-__device__ __forceinline__ void epilogue_store(const EpiParams& ep, const uint32_t (&v)[32],
-                                               int row, int n) {
-    int32_t acc[32];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) acc[i] = kInt4 ? ((int32_t)v[i] >> 8) : (int32_t)v[i];
-    uint8_t* orow = reinterpret_cast<uint8_t*>(ep.out) + (int64_t)row * ep.ldo_bytes;
-    if (ep.mode == OUT_I32) {
-        int4* o = reinterpret_cast<int4*>(orow + (int64_t)n * 4);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) o[i] = make_int4(acc[4 * i], acc[4 * i + 1], acc[4 * i + 2], acc[4 * i + 3]);
-        return;
-    }
-    float y[32];
-    const bool hb = ep.bias != nullptr;
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
-        const float sc = __fmul_rn(ep.s_a, __ldg(ep.s_w + n + i));
-        const float b = hb ? __ldg(ep.bias + n + i) : 0.0f;
-        y[i] = dequant(acc[i], sc, b, hb);
-    }
+// y (dequant [+GELU]) -> the output mode's encoding, one row, 32 columns.
+__device__ __forceinline__ void epilogue_emit(const EpiParams& ep, float (&y)[32], uint8_t* orow, int n) {
     if (ep.gelu) {
 #pragma unroll
         for (int i = 0; i < 32; ++i) y[i] = gelu_pinned(y[i]);
@@ -148,11 +130,62 @@ __device__ __forceinline__ void epilogue_store(const EpiParams& ep, const uint32
     }
 }
 
+// Exact int32 sums acc[32] of one row -> dequant (R4) with the per-column
+// sc = fl(s_a s_w[n]) and bias read from `sc`/`bb` (global via __ldg, or
+// shared memory), then the output encoding.
+template <bool kSmemScales>
+__device__ __forceinline__ void epilogue_acc(const EpiParams& ep, const int32_t (&acc)[32], int row, int n,
+                                             const float* sc_s, const float* b_s) {
+    uint8_t* orow = reinterpret_cast<uint8_t*>(ep.out) + (int64_t)row * ep.ldo_bytes;
+    if (ep.mode == OUT_I32) {
+        int4* o = reinterpret_cast<int4*>(orow + (int64_t)n * 4);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i] = make_int4(acc[4 * i], acc[4 * i + 1], acc[4 * i + 2], acc[4 * i + 3]);
+        return;
+    }
+    float y[32];
+    const bool hb = ep.bias != nullptr;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+        const float sc = kSmemScales ? sc_s[i] : __fmul_rn(ep.s_a, __ldg(ep.s_w + n + i));
+        const float b = kSmemScales ? b_s[i] : (hb ? __ldg(ep.bias + n + i) : 0.0f);
+        y[i] = dequant(acc[i], sc, b, hb);
+    }
+    epilogue_emit(ep, y, orow, n);
+}
+
+template <bool kInt4>
+__device__ __forceinline__ void epilogue_store(const EpiParams& ep, const uint32_t (&v)[32], int row, int n) {
+    int32_t acc[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) acc[i] = kInt4 ? ((int32_t)v[i] >> 8) : (int32_t)v[i];
+    epilogue_acc<false>(ep, acc, row, n, nullptr, nullptr);
+}
+
+#ifdef MKQ_TTRACE
+// Diagnostics build only (tools/trace_small.py): per-CTA (globaltimer,
+// clock64) at fixed points of the 1-CTA GEMM.
+__device__ unsigned long long* g_ttrace = nullptr;
+#define TTRACE(slot)                                                                        \
+    do {                                                                                    \
+        if (g_ttrace && blockIdx.x < 256) {                                                  \
+            unsigned long long gt;                                                          \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));                          \
+            g_ttrace[(blockIdx.x * 16 + (slot)) * 2] = gt;                                   \
+            g_ttrace[(blockIdx.x * 16 + (slot)) * 2 + 1] = clock64();                        \
+        }                                                                                   \
+    } while (0)
+#else
+#define TTRACE(slot) \
+    do {             \
+    } while (0)
+#endif
+
 // ------------------------------------------------------------------ kernel
-template <class Cfg>
+template <class Cfg, bool kCl = false>
 __global__ void __launch_bounds__(Cfg::kThreads, 1)
     gemm_i8tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     const EpiParams ep, int M, int N, int K) {
+                     const EpiParams ep, int M, int N, int K, int splits) {
     constexpr int BM = Cfg::BM, BN = Cfg::BN, S8 = Cfg::S8, SP = Cfg::SP;
     constexpr bool kInt4 = Cfg::kInt4;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -170,10 +203,26 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) TTRACE(0);
     const int m_tiles = (M + BM - 1) / BM;
     const int n_tiles = (N + BN - 1) / BN;
-    const int num_tiles = m_tiles * n_tiles;
+    // Work units: (output tile, K split).  kCl (the small-M plan, SURVEY §8f
+    // NEXT(1)): one unit per CTA, the `splits` CTAs of a thread-block cluster
+    // share one output tile and each accumulates a K range; the exact int32
+    // partials are staged in shared memory and reduce-scattered over DSMEM
+    // (CTA r sums rows r*BM/splits.. of every peer -- integer addition, so
+    // the result is exact in any order, R15) and all warps run the epilogue
+    // of their row slice.  Otherwise (splits == 1) persistent over tiles.
+    const int num_tiles = m_tiles * n_tiles * splits;
     const int nk = (K + Cfg::BK - 1) / Cfg::BK;
+    auto k_range = [&](int unit, int& kb0, int& kb1) {
+        const int ks = unit % splits;
+        kb0 = (int)((int64_t)ks * nk / splits);
+        kb1 = (int)((int64_t)(ks + 1) * nk / splits);
+    };
+    constexpr int kRP = Cfg::BN * 4 + 16;   // staged partial row pitch (bytes)
+    static_assert(!kCl || Cfg::BM * kRP <= Cfg::S8 * Cfg::kStage8, "partial staging fits the int8 ring");
+    __shared__ float sc_s[kCl ? Cfg::BN : 1], b_s[kCl ? Cfg::BN : 1];
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < S8; ++i) {
@@ -199,21 +248,27 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if (threadIdx.x == 0) TTRACE(1);
 
     if (warp == 0) {
         // ---------------------------------------------------- TMA producer
         if (lane == 0) {
             int s = 0;
             uint32_t ph = 0;
-            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            for (int unit = blockIdx.x; unit < num_tiles; unit += gridDim.x) {
+                const int tile = unit / splits;
                 const int m0 = (tile / n_tiles) * BM, n0 = (tile % n_tiles) * BN;
-                for (int kb = 0; kb < nk; ++kb) {
+                int kb0, kb1;
+                k_range(unit, kb0, kb1);
+                for (int kb = kb0; kb < kb1; ++kb) {
                     if constexpr (kInt4) {
                         ptx::mbar_wait(&emptyP[s], ph ^ 1);
                         uint8_t* dst = ringP + s * Cfg::kStageP;
                         ptx::mbar_arrive_expect_tx(&fullP[s], Cfg::kStageP);
                         ptx::tma_load_2d(&tmA, &fullP[s], dst, kb * (Cfg::BK / 2), m0);
                         ptx::tma_load_2d(&tmB, &fullP[s], dst + Cfg::kAP, kb * (Cfg::BK / 2), n0);
+                        if (kb == kb0) TTRACE(2);
+                        if (kb == kb0 + 4) TTRACE(3);
                         if (++s == SP) { s = 0; ph ^= 1; }
                     } else {
                         ptx::mbar_wait(&empty8[s], ph ^ 1);
@@ -241,20 +296,25 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
             int s = 0;
             uint32_t ph = 0;
             int it = 0;
-            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+            for (int unit = blockIdx.x; unit < num_tiles; unit += gridDim.x, ++it) {
                 const int ab = it & 1;
                 const uint32_t aph = (it >> 1) & 1;
                 ptx::mbar_wait(&tempty[ab], aph ^ 1);
                 ptx::tc_fence_after();
                 const uint32_t d = tmem_base + ab * BN;
-                for (int kb = 0; kb < nk; ++kb) {
+                int kb0, kb1;
+                k_range(unit, kb0, kb1);
+                for (int kb = kb0; kb < kb1; ++kb) {
                     ptx::mbar_wait(&full8[s], ph);
                     ptx::tc_fence_after();
+                    if (lane == 0 && kb == kb0) TTRACE(4);
+                    if (lane == 0 && kb == kb1 - 1) TTRACE(5);
+                    if (lane == 0 && kb > kb0 && kb - kb0 < 7) TTRACE(9 + kb - kb0);
                     const uint64_t da = dA0 + (uint64_t)((s * Cfg::kStage8) >> 4);
                     const uint64_t db = da + (uint64_t)(Cfg::kA8 >> 4);
 #pragma unroll
                     for (int k = 0; k < Cfg::BK / 32; ++k)
-                        ptx::mma_i8_ss_warp(d, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+                        ptx::mma_i8_ss_warp(d, da + 2 * k, db + 2 * k, idesc, (kb != kb0) || k != 0);
                     ptx::mma_commit_warp(&empty8[s]);
                     if (++s == S8) { s = 0; ph ^= 1; }
                 }
@@ -265,12 +325,14 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
         // ---------------------------------------------------- epilogue
         const int q = warp & 3;   // TMEM lane quadrant owned by this warp
         int it = 0;
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+        for (int unit = blockIdx.x; unit < num_tiles; unit += gridDim.x, ++it) {
+            const int tile = unit / splits;
             const int m0 = (tile / n_tiles) * BM, n0 = (tile % n_tiles) * BN;
             const int ab = it & 1;
             const uint32_t aph = (it >> 1) & 1;
             ptx::mbar_wait(&tfull[ab], aph);
             ptx::tc_fence_after();
+            if (threadIdx.x == 128) TTRACE(6);
             const int row = m0 + q * 32 + lane;
 #pragma unroll 1
             for (int j = 0; j < BN / 32; ++j) {
@@ -279,10 +341,33 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
                 uint32_t v[32];
                 ptx::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + ab * BN + 32 * j, v);
                 ptx::tmem_ld_wait();
-                if (row < M) epilogue_store<kInt4>(ep, v, row, n);
+                if constexpr (kCl) {
+                    // stage the (shifted) partial of row q*32+lane in the idle int8 ring
+                    uint8_t* dst = ring8 + (q * 32 + lane) * kRP + j * 128;
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        uint4 t;
+                        t.x = kInt4 ? (uint32_t)((int32_t)v[4 * i] >> 8) : v[4 * i];
+                        t.y = kInt4 ? (uint32_t)((int32_t)v[4 * i + 1] >> 8) : v[4 * i + 1];
+                        t.z = kInt4 ? (uint32_t)((int32_t)v[4 * i + 2] >> 8) : v[4 * i + 2];
+                        t.w = kInt4 ? (uint32_t)((int32_t)v[4 * i + 3] >> 8) : v[4 * i + 3];
+                        *reinterpret_cast<uint4*>(dst + 16 * i) = t;
+                    }
+                } else if (row < M) {
+                    epilogue_store<kInt4>(ep, v, row, n);
+                }
             }
             ptx::tc_fence_before();
             ptx::mbar_arrive(&tempty[ab]);
+            if (threadIdx.x == 128) TTRACE(7);
+        }
+    } else if (kCl && warp == 3) {
+        // ---------------------------------------------------- scale/bias prefetch
+        const int n0 = ((blockIdx.x / splits) % n_tiles) * BN;
+        for (int c = lane; c < BN; c += 32) {
+            const int n = n0 + c;
+            sc_s[c] = n < N ? __fmul_rn(ep.s_a, __ldg(ep.s_w + n)) : 0.0f;
+            b_s[c] = (n < N && ep.bias) ? __ldg(ep.bias + n) : 0.0f;
         }
     } else if (kInt4 && warp >= 8) {
         // ---------------------------------------------------- int4 -> int8 unpack
@@ -291,8 +376,10 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
         static_assert(kChunks % 128 == 0, "chunk split");
         int sp = 0, s8 = 0;
         uint32_t php = 0, ph8 = 0;
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-            for (int kb = 0; kb < nk; ++kb) {
+        for (int unit = blockIdx.x; unit < num_tiles; unit += gridDim.x) {
+            int kb0, kb1;
+            k_range(unit, kb0, kb1);
+            for (int kb = kb0; kb < kb1; ++kb) {
                 ptx::mbar_wait(&fullP[sp], php);
                 ptx::mbar_wait(&empty8[s8], ph8 ^ 1);
                 const uint8_t* src = ringP + sp * Cfg::kStageP;
@@ -325,8 +412,47 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
         }
     }
 
+    if constexpr (kCl) {
+        // DSMEM reduce-scatter of the staged partials + epilogue (all warps)
+        ptx::cluster_sync();   // release/acquire: every peer's staged rows are visible
+        const int tile = blockIdx.x / splits;
+        const int m0 = (tile / n_tiles) * BM, n0 = (tile % n_tiles) * BN;
+        const int rank = (int)ptx::cluster_ctarank();
+        const int rows_per = (BM + splits - 1) / splits;
+        const int r0 = rank * rows_per, r1 = min(BM, r0 + rows_per);
+        constexpr int kJ = BN / 32;
+        const int tasks = (r1 - r0) * kJ;
+        const uint32_t red0 = ptx::smem_u32(ring8);
+        for (int t = threadIdx.x; t < tasks; t += blockDim.x) {
+            const int rl = r0 + t / kJ, j = t % kJ;
+            const int row = m0 + rl, n = n0 + 32 * j;
+            if (row >= M || n >= N) continue;
+            int32_t acc[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) acc[i] = 0;
+            // all 8 loads of a peer in flight before any add (in-order issue)
+            for (int sp = 0; sp < splits; ++sp) {
+                uint32_t ra;
+                asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(red0 + rl * kRP + j * 128), "r"(sp));
+                uint4 x[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    asm volatile("ld.shared::cluster.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                 : "=r"(x[i].x), "=r"(x[i].y), "=r"(x[i].z), "=r"(x[i].w) : "r"(ra + 16 * i));
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    acc[4 * i] += (int32_t)x[i].x; acc[4 * i + 1] += (int32_t)x[i].y;
+                    acc[4 * i + 2] += (int32_t)x[i].z; acc[4 * i + 3] += (int32_t)x[i].w;
+                }
+            }
+            epilogue_acc<true>(ep, acc, row, n, sc_s + 32 * j, b_s + 32 * j);
+        }
+        if (threadIdx.x == 128) TTRACE(8);
+        ptx::cluster_sync();   // peers may still be reading this CTA's rows
+    }
     ptx::tc_fence_before();
     __syncthreads();
+    if (threadIdx.x == 0) TTRACE(9);
     if (warp == 2) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc<Cfg::kTmemCols>(tmem_base);

@@ -10,6 +10,7 @@
 #include <cstring>
 #include <cstdlib>
 #include <algorithm>
+#include <atomic>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -27,6 +28,13 @@
 #include "calib.cuh"
 
 #define MKQ_VERSION 10000
+
+#ifdef MKQ_TTRACE
+extern "C" __attribute__((visibility("default"))) int mkq_debug_set_ttrace(void* p) {
+    unsigned long long* q = static_cast<unsigned long long*>(p);
+    return (int)cudaMemcpyToSymbol(mkq::g_ttrace, &q, sizeof(q));
+}
+#endif
 
 namespace {
 
@@ -157,15 +165,15 @@ mkq_status make_out_map(CUtensorMap* out, void* base, int mode, int64_t M, int64
 }
 
 // ------------------------------------------------------------------ GEMM dispatch
-template <class Cfg>
+template <class Cfg, bool kCl = false>
 mkq_status launch_gemm(const void* a, int64_t lda, const void* w, int64_t ldw, int M, int N, int K,
-                       const mkq::EpiParams& ep, int sms, cudaStream_t st) {
+                       const mkq::EpiParams& ep, int sms, cudaStream_t st, int splits = 1) {
     static bool attr_set[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
     if (!attr_set[dev]) {
-        cudaError_t e = cudaFuncSetAttribute(mkq::gemm_i8tc_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             Cfg::kSmem);
+        cudaError_t e = cudaFuncSetAttribute(mkq::gemm_i8tc_kernel<Cfg, kCl>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
         if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
         attr_set[dev] = true;
     }
@@ -177,9 +185,27 @@ mkq_status launch_gemm(const void* a, int64_t lda, const void* w, int64_t ldw, i
     s = make_map(&mb, w, kbytes, (uint64_t)N, (uint64_t)ldw, box_in, Cfg::BN, !Cfg::kInt4);
     if (s != MKQ_OK) return s;
     const int tiles = ((M + Cfg::BM - 1) / Cfg::BM) * ((N + Cfg::BN - 1) / Cfg::BN);
-    const int grid = tiles < sms ? tiles : sms;
-    mkq::gemm_i8tc_kernel<Cfg><<<grid, Cfg::kThreads, Cfg::kSmem, st>>>(ma, mb, ep, M, N, K);
-    cudaError_t e = cudaPeekAtLastError();
+    cudaError_t e;
+    if constexpr (kCl) {
+        // one CTA per (tile, K split); the splits of a tile form one cluster
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(tiles * splits));
+        cfg.blockDim = dim3(Cfg::kThreads);
+        cfg.dynamicSmemBytes = Cfg::kSmem;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = (unsigned)splits;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        e = cudaLaunchKernelEx(&cfg, mkq::gemm_i8tc_kernel<Cfg, true>, ma, mb, ep, M, N, K, splits);
+    } else {
+        const int grid = tiles < sms ? tiles : sms;
+        mkq::gemm_i8tc_kernel<Cfg, false><<<grid, Cfg::kThreads, Cfg::kSmem, st>>>(ma, mb, ep, M, N, K, 1);
+        e = cudaPeekAtLastError();
+    }
     if (e != cudaSuccess) return cuda_fail(e, "gemm launch");
     return MKQ_OK;
 }
@@ -217,6 +243,90 @@ mkq_status launch_gemm2(const void* a, int64_t lda, const void* w, int64_t ldw, 
     cudaError_t e = cudaPeekAtLastError();
     if (e != cudaSuccess) return cuda_fail(e, "gemm2 launch");
     return MKQ_OK;
+}
+
+// Small-M plan (the paper's Table 2 regime of a few
+// hundred to a few thousand valid tokens): when the large-tile paths would
+// leave most SMs idle, the 1-CTA kernel runs 128 x 64 tiles and splits K over
+// the CTAs of a thread-block cluster so that about one work unit lands on
+// every SM; the partials are reduced through distributed shared memory.
+// Exact: the split partials are int32 and are summed as integers (R15).
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct SmallPlan {
+    bool use = false;
+    int bn = 64;
+    int splits = 1;
+    int64_t tiles = 0;
+};
+
+// -1 heuristic (default), 0 never, 1 always: mkq_set_small_m_mode() or the
+// MKQ_SMALL_M environment variable (tests and diagnostics).
+std::atomic<int> g_small_mode{[] { const char* e = getenv("MKQ_SMALL_M"); return e ? atoi(e) : -1; }()};
+
+// cudaOccupancyMaxActiveClusters of the small-M kernel per cluster size
+// (cached per device; int4 and int8 variants use the same shared memory
+// class, one CTA per SM).
+int max_clusters(int csize) {
+    static int cache[64][9] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64 || csize < 1 || csize > 8) return 0;
+    int& c = cache[dev][csize];
+    if (c == 0) {
+        using Cfg = mkq::GemmCfg<64, true>;
+        cudaFuncSetAttribute(mkq::gemm_i8tc_kernel<Cfg, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(csize * 64));
+        cfg.blockDim = dim3(Cfg::kThreads);
+        cfg.dynamicSmemBytes = Cfg::kSmem;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = (unsigned)csize;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, mkq::gemm_i8tc_kernel<Cfg, true>, &cfg) != cudaSuccess || n < 1) {
+            cudaGetLastError();
+            n = 1;
+        }
+        c = n;
+    }
+    return c;
+}
+
+int small_m_mode() { return g_small_mode.load(std::memory_order_relaxed); }
+
+// Single wave only: 128 x 64 tiles if they fit one per SM, else the
+// large-tile paths.  K is split over a cluster while the clusters
+// still fit (one wave, <= 4 CTAs per cluster, >= 2 K-blocks per split).
+SmallPlan plan_small(int64_t M, int64_t N, int64_t K, int sms) {
+    SmallPlan p;
+    const int mode = small_m_mode();
+    if (mode == 0) return p;
+    const int64_t mt = (M + 127) / 128;
+    const int64_t t64 = mt * ((N + 63) / 64), t128 = mt * ((N + 127) / 128);
+    // (128 x 128 tiles measured slower than the 2-CTA 256 x 256 path at
+    // Table-2 sizes: t64 > sms goes to the large-tile paths)
+    (void)t128;
+    if (t64 <= sms || mode == 1) {
+        p.bn = 64;
+        p.tiles = t64;
+    } else {
+        return p;
+    }
+    p.use = true;
+    const int64_t nk = (K + 127) / 128;
+    int64_t sp = sms / std::max<int64_t>(p.tiles, 1);
+    sp = std::min<int64_t>(sp, nk / 2);   // >= 2 K-blocks per split
+    static const int max_split = [] { const char* e = getenv("MKQ_MAX_SPLIT"); return e ? atoi(e) : 4; }();
+    sp = std::min<int64_t>(sp, max_split);   // clusters of <= 4 full-SM CTAs co-reside in a GPC
+    p.splits = (int)std::max<int64_t>(sp, 1);
+    // every cluster must be co-resident (one wave)
+    while (p.splits > 1 && p.tiles > max_clusters(p.splits)) --p.splits;
+    return p;
 }
 
 mkq_status gemm_common(bool int4, const void* a, int64_t lda, const void* w, int64_t ldw, int64_t M, int64_t N,
@@ -269,6 +379,15 @@ mkq_status gemm_common(bool int4, const void* a, int64_t lda, const void* w, int
     ep.out = out;
     ep.ldo_bytes = ldo;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const SmallPlan sp = plan_small(M, N, K, sms);
+    if (sp.use) {
+        if (sp.bn == 128) {
+            if (int4) return launch_gemm<mkq::GemmCfg<128, true>, true>(a, lda, w, ldw, (int)M, (int)N, (int)K, ep, sms, st, sp.splits);
+            return launch_gemm<mkq::GemmCfg<128, false>, true>(a, lda, w, ldw, (int)M, (int)N, (int)K, ep, sms, st, sp.splits);
+        }
+        if (int4) return launch_gemm<mkq::GemmCfg<64, true>, true>(a, lda, w, ldw, (int)M, (int)N, (int)K, ep, sms, st, sp.splits);
+        return launch_gemm<mkq::GemmCfg<64, false>, true>(a, lda, w, ldw, (int)M, (int)N, (int)K, ep, sms, st, sp.splits);
+    }
     const bool wide = (N % 256 == 0) && (M > 128 * sms / 2 || (M / 128 + 1) * (N / 256) >= sms);
     static const int path_override = [] {   // MKQ_GEMM_PATH=1cta|2cta (diagnostics)
         const char* v = getenv("MKQ_GEMM_PATH");
@@ -309,7 +428,6 @@ int grid_for(int64_t work, int threads, int sms) {
     return (int)g;
 }
 
-size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 // Launch the quantize/pack kernels; the scale is a device pointer (scale_dev)
 // or, when that is NULL, the per-tensor value s_val.  Arguments validated.
@@ -415,6 +533,8 @@ mkq_status mkq_gemm_w8a8(const void* a, int64_t lda, const void* w, int64_t ldw,
                          int64_t ldo, void* ws, size_t ws_bytes, void* stream) {
     return gemm_common(false, a, lda, w, ldw, M, N, K, s_a, s_w, bias, epi, out, ldo, ws, ws_bytes, stream);
 }
+
+void mkq_set_small_m_mode(int mode) { g_small_mode.store(mode < 0 ? -1 : (mode ? 1 : 0)); }
 
 size_t mkq_gemm_workspace_size(int64_t, int64_t, int64_t) { return 0; }
 

@@ -124,6 +124,23 @@ def mkq_requant_table(gelu: bool, s_out: float, qmin: int, qmax: int, device=Non
     return t
 
 
+_GEMM_WS = {}
+
+
+def _gemm_ws(M: int, N: int, K: int, device, stream):
+    """Split-K scratch for small-M GEMMs (mkq_gemm_workspace_size), one
+    cached buffer per (device, stream): calls on one stream are ordered."""
+    nb = int(lib().mkq_gemm_workspace_size(M, N, K))
+    if nb == 0:
+        return None
+    key = (str(device), _stream(stream).value)
+    buf = _GEMM_WS.get(key)
+    if buf is None or buf.numel() < nb:
+        buf = torch.empty(nb, dtype=torch.uint8, device=device)
+        _GEMM_WS[key] = buf
+    return buf
+
+
 def _gemm(name: str, a, w, K: int, s_a: float, s_w, bias, mode: int, gelu: bool, s_out: float, qmin: int,
           qmax: int, out, stream, requant_table=None):
     M, N = a.shape[0], w.shape[0]
@@ -136,8 +153,10 @@ def _gemm(name: str, a, w, K: int, s_a: float, s_w, bias, mode: int, gelu: bool,
     epi = MkqEpilogue(mode, int(gelu), float(s_out), qmin, qmax,
                       None if requant_table is None else requant_table.data_ptr())
     fn = getattr(lib(), name)
+    ws = _gemm_ws(M, N, K, a.device, stream)
     check(name, fn(_ptr(a), _row_bytes(a), _ptr(w), _row_bytes(w), M, N, K, float(s_a), _ptr(s_w), _ptr(bias),
-                   ctypes.byref(epi), _ptr(out), _row_bytes(out), None, 0, _stream(stream)))
+                   ctypes.byref(epi), _ptr(out), _row_bytes(out), _ptr(ws), 0 if ws is None else ws.numel(),
+                   _stream(stream)))
     return out
 
 

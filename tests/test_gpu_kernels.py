@@ -85,19 +85,60 @@ SHAPES = [(1, 32, 32), (7, 64, 96), (128, 768, 768), (129, 256, 160), (300, 512,
           (1000, 3072, 768)]
 
 
+@pytest.fixture(params=[-1, 0, 1], ids=["plan-auto", "plan-large", "plan-small"])
+def small_mode(request):
+    """GEMM tile plan: heuristic, never / always the small-M split-K plan."""
+    from paper_2203_13483_b200._lib import lib
+    lib().mkq_set_small_m_mode(request.param)
+    yield request.param
+    lib().mkq_set_small_m_mode(-1)
+
+
 @pytest.mark.parametrize("bits", [4, 8])
 @pytest.mark.parametrize("Mm,N,K", SHAPES)
-def test_gemm_raw_i32_bitexact(bits, Mm, N, K):
+def test_gemm_raw_i32_bitexact(bits, Mm, N, K, small_mode):
     rng = np.random.default_rng(Mm * 31 + N + K)
     A, W = _codes(rng, Mm, N, K, bits)
     out = _run(bits, A, W, 1.0, np.ones(N, np.float32), None, mode=M.OUT_I32)
     assert np.array_equal(host(out), oracle.gemm_i32(A, W))
 
 
+# Table-2 sized GEMMs (BERT-base, 440 / 2298 valid tokens) through the small-M
+# split-K plan, every epilogue mode, repeated calls (self-resetting counters)
+@pytest.mark.parametrize("bits", [4, 8])
+@pytest.mark.parametrize("Mm,N,K", [(440, 768, 3072), (440, 2304, 768), (440, 3072, 768), (440, 768, 768),
+                                     (1, 768, 3072), (130, 64, 4096), (2298, 768, 768)])
+def test_gemm_small_m_split_k(bits, Mm, N, K):
+    from paper_2203_13483_b200._lib import lib
+    lib().mkq_set_small_m_mode(1)
+    try:
+        rng = np.random.default_rng(Mm + N + K + bits)
+        A, W = _codes(rng, Mm, N, K, bits)
+        ref = oracle.gemm_i32(A, W)
+        for _ in range(3):
+            assert np.array_equal(host(_run(bits, A, W, 1.0, np.ones(N, np.float32), None, mode=M.OUT_I32)), ref)
+        lo, hi = (-8, 7) if bits == 4 else (-128, 127)
+        s_a = np.float32(0.31 if bits == 4 else 0.0306)
+        s_w = rng.uniform(1e-3, 5e-3, N).astype(np.float32)
+        b = rng.uniform(-0.1, 0.1, N).astype(np.float32)
+        out = host(_run(bits, A, W, s_a, s_w, b, mode=M.OUT_F32))
+        assert np.array_equal(out.view(np.uint32), oracle.linear(A, W, s_a, s_w, b).view(np.uint32))
+        s_out = np.float32(0.05 if bits == 4 else 0.004)
+        mode = M.OUT_I4 if bits == 4 else M.OUT_I8
+        r = oracle.linear(A, W, s_a, s_w, b, mode=oracle.OUT_I4 if bits == 4 else oracle.OUT_I8, gelu=True,
+                          s_out=s_out, qmin_out=lo, qmax_out=hi)
+        for table in (True, False):   # exact requant table / direct GELU + division
+            out = host(_run(bits, A, W, s_a, s_w, b, mode=mode, gelu=True, s_out=s_out, qmin=lo, qmax=hi,
+                            requant_table=table))
+            assert np.array_equal(out, oracle.pack_int4(r)) if bits == 4 else np.array_equal(out.view(np.int8), r)
+    finally:
+        lib().mkq_set_small_m_mode(-1)
+
+
 @pytest.mark.parametrize("bits", [4, 8])
 @pytest.mark.parametrize("mode", [M.OUT_F32, M.OUT_F16, M.OUT_BF16])
 @pytest.mark.parametrize("gelu", [False, True])
-def test_gemm_float_epilogues_bitexact(bits, mode, gelu):
+def test_gemm_float_epilogues_bitexact(bits, mode, gelu, small_mode):
     rng = np.random.default_rng(17 + mode)
     Mm, N, K = 300, 768, 1024
     A, W = _codes(rng, Mm, N, K, bits)
@@ -115,7 +156,7 @@ def test_gemm_float_epilogues_bitexact(bits, mode, gelu):
 
 @pytest.mark.parametrize("bits", [4, 8])
 @pytest.mark.parametrize("Mm,N,K", [(1, 32, 64), (128, 3072, 768), (257, 4096, 1024)])
-def test_gemm_requant_gelu_bitexact(bits, Mm, N, K):
+def test_gemm_requant_gelu_bitexact(bits, Mm, N, K, small_mode):
     rng = np.random.default_rng(5 + Mm)
     A, W = _codes(rng, Mm, N, K, bits)
     lo, hi = (-8, 7) if bits == 4 else (-128, 127)
