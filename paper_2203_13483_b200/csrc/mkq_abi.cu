@@ -634,12 +634,19 @@ mkq_status mkq_attention(const void* qkv, int64_t ld, int64_t batch, int64_t max
     }
     mkq_status s = check_device();
     if (s != MKQ_OK) return s;
-    static const int attn_path = [] {   // MKQ_ATTN=tc|mma select the older kernels (diagnostics)
+    static const int attn_env = [] {   // MKQ_ATTN=tc|mma|pp forces a kernel (diagnostics)
         const char* v = getenv("MKQ_ATTN");
         if (v && strcmp(v, "mma") == 0) return 1;
         if (v && strcmp(v, "tc") == 0) return 0;
-        return 2;
+        if (v && strcmp(v, "pp") == 0) return 2;
+        return -1;
     }();
+    // Short sequences (max_seq <= 128: BERT-base configs, the paper's Table 2
+    // batches of ~30 valid tokens per sequence): the mma.sync flash kernel,
+    // 64-query CTAs that exit early past the sequence end, beats the
+    // persistent tcgen05 kernel's 2 x 128-query tiles (6.6 vs 11.2 us at 440
+    // valid tokens, 12.7 vs 28.7 us at 2298); long sequences: tcgen05.
+    const int attn_path = attn_env >= 0 ? attn_env : (max_seq <= 128 ? 1 : 2);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (attn_path == 2) {
         const int mi = out_mode == MKQ_OUT_F32 ? 0 : (out_mode == MKQ_OUT_I4 ? 1 : 2);

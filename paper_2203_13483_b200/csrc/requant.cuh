@@ -225,17 +225,32 @@ __global__ void finalize4_kernel(Header* h, Header4* h4, uint32_t* cells4, const
     if (!(v.a >= 0.0f && v.a < 3.0e38f)) ok = false;
     int run = h->code_lo;
     int p = 0;
+    // A cell may hold a cluster of change points (gelu_pinned(y)/s is not
+    // monotone at the ulp level, so a code can flicker c, c+1, c, c+1 over a
+    // few floats): one word covers it when every point of the cluster lies in
+    // the word's +-511-ulp window, where the epilogue evaluates directly;
+    // below / above the window the codes are the cluster's first "before"
+    // and last "after" (the verify pass re-checks every float).
+    auto in_win = [](uint32_t b, uint32_t wb) { return b - wb + 511u < 1023u; };
     for (int i = 0; i < kCells4 && ok; ++i) {
         uint32_t w = 0x7F800000u | (uint32_t)(run & 0xF) * 0x11u;
+        const int before = run;
         int cnt = 0;
+        uint32_t fb = 0, lb = 0;
         while (p < n && (int)cell4(chg[p].y, v.a, v.b) == i) {
             if (chg[p].before != run) ok = false;
-            w = (__float_as_uint(chg[p].y) & ~0x1FFu) | (uint32_t)(run & 0xF) | ((uint32_t)(chg[p].after & 0xF) << 4);
+            if (cnt == 0) fb = __float_as_uint(chg[p].y);
+            lb = __float_as_uint(chg[p].y);
             run = chg[p].after;
             ++cnt;
             ++p;
         }
-        if (cnt > 1) ok = false;
+        if (cnt >= 1) {
+            uint32_t wb = fb & ~0x1FFu;
+            if (!(in_win(fb, wb) && in_win(lb, wb))) wb = lb & ~0x1FFu;
+            if (!(in_win(fb, wb) && in_win(lb, wb))) ok = false;
+            w = wb | (uint32_t)(before & 0xF) | ((uint32_t)(run & 0xF) << 4);
+        }
         cells4[i] = w;
     }
     if (run != h->code_hi || p != n) ok = false;
