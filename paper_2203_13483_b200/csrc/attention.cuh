@@ -92,6 +92,7 @@ struct Params {
 };
 
 __global__ void __launch_bounds__(kThreads) flash_attn_kernel(const Params p) {
+    asm volatile("griddepcontrol.launch_dependents;\n\tgriddepcontrol.wait;" ::: "memory");   // PDL (ptx.cuh)
     __shared__ __align__(128) uint8_t smem[kBQ * 128 + 4 * kBK * 128];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int head = blockIdx.y, b = blockIdx.z;

@@ -138,6 +138,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0) ptx::tmem_alloc<512>(tmem_slot);
     ptx::tc_fence_before();
     __syncthreads();
+    ptx::pdl_launch();
+    ptx::pdl_wait();
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     // S_x = tmem + x*kBK, O_x = tmem + 2*kBK + x*kD, P_x = tmem + 2*kBK + (2+x)*kD

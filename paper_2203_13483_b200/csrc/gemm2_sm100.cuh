@@ -405,6 +405,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
     ptx::tc_fence_before();
     ptx::cluster_sync();
     __syncthreads();   // CTA barrier as well (orders the slot write for tools that do not model barrier.cluster)
+    ptx::pdl_launch();
+    ptx::pdl_wait();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     // kLut4: register reallocation per warpgroup (each executes one setmaxnreg

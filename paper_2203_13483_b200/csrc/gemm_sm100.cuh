@@ -248,6 +248,8 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    ptx::pdl_launch();
+    ptx::pdl_wait();
     if (threadIdx.x == 0) TTRACE(1);
 
     if (warp == 0) {

@@ -23,6 +23,7 @@ __global__ void __launch_bounds__(256) residual_ln_kernel(
     const float* __restrict__ x, const float* __restrict__ res, int64_t rows, int cols, int64_t ld,
     const float* __restrict__ g, const float* __restrict__ b, float eps, float* __restrict__ y,
     int bits, float s_q, int qmin, int qmax, uint8_t* __restrict__ q, int64_t ldq) {
+    asm volatile("griddepcontrol.launch_dependents;\n\tgriddepcontrol.wait;" ::: "memory");   // PDL (ptx.cuh)
     const int lane = threadIdx.x & 31;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
     const int nv = cols >> 2;

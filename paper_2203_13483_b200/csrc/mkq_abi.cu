@@ -14,6 +14,7 @@
 #include <map>
 #include <mutex>
 #include <tuple>
+#include <utility>
 
 #include "../../include/mkq.h"
 #include "attention.cuh"
@@ -50,6 +51,41 @@ mkq_status fail(mkq_status s, const char* fmt, ...) {
 
 mkq_status cuda_fail(cudaError_t e, const char* what) {
     return fail(MKQ_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+// Launch with programmatic dependent launch (PDL, griddepcontrol in the
+// kernels) so a kernel's prologue overlaps the previous kernel's tail; in a
+// CUDA graph the attribute becomes a programmatic edge.  MKQ_PDL=0 disables.
+bool pdl_enabled() {
+    static const bool on = [] { const char* e = getenv("MKQ_PDL"); return !(e && strcmp(e, "0") == 0); }();
+    return on;
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, int cluster,
+                     Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    int n = 0;
+    if (pdl_enabled()) {
+        at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[n].val.programmaticStreamSerializationAllowed = 1;
+        ++n;
+    }
+    if (cluster > 1) {
+        at[n].id = cudaLaunchAttributeClusterDimension;
+        at[n].val.clusterDim.x = (unsigned)cluster;
+        at[n].val.clusterDim.y = 1;
+        at[n].val.clusterDim.z = 1;
+        ++n;
+    }
+    cfg.attrs = at;
+    cfg.numAttrs = n;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
 bool finite_pos(float s) { return std::isfinite(s) && s > 0.0f; }
@@ -188,23 +224,12 @@ mkq_status launch_gemm(const void* a, int64_t lda, const void* w, int64_t ldw, i
     cudaError_t e;
     if constexpr (kCl) {
         // one CTA per (tile, K split); the splits of a tile form one cluster
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3((unsigned)(tiles * splits));
-        cfg.blockDim = dim3(Cfg::kThreads);
-        cfg.dynamicSmemBytes = Cfg::kSmem;
-        cfg.stream = st;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = (unsigned)splits;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        e = cudaLaunchKernelEx(&cfg, mkq::gemm_i8tc_kernel<Cfg, true>, ma, mb, ep, M, N, K, splits);
+        e = launch_k(mkq::gemm_i8tc_kernel<Cfg, true>, dim3((unsigned)(tiles * splits)), dim3(Cfg::kThreads),
+                     Cfg::kSmem, st, splits, ma, mb, ep, M, N, K, splits);
     } else {
         const int grid = tiles < sms ? tiles : sms;
-        mkq::gemm_i8tc_kernel<Cfg, false><<<grid, Cfg::kThreads, Cfg::kSmem, st>>>(ma, mb, ep, M, N, K, 1);
-        e = cudaPeekAtLastError();
+        e = launch_k(mkq::gemm_i8tc_kernel<Cfg, false>, dim3(grid), dim3(Cfg::kThreads), Cfg::kSmem, st, 1, ma, mb,
+                     ep, M, N, K, 1);
     }
     if (e != cudaSuccess) return cuda_fail(e, "gemm launch");
     return MKQ_OK;
@@ -239,8 +264,8 @@ mkq_status launch_gemm2(const void* a, int64_t lda, const void* w, int64_t ldw, 
     static const int max_cl = [] { const char* v = getenv("MKQ_MAX_CLUSTERS"); return v ? atoi(v) : 0; }();
     int clusters = tiles < sms / 2 ? tiles : sms / 2;
     if (max_cl > 0 && clusters > max_cl) clusters = max_cl;
-    mkq::gemm_w4a4_2cta_kernel<Cfg><<<2 * clusters, Cfg::kThreads, Cfg::kSmem, st>>>(ma, mb, mo, ep, M, N, K);
-    cudaError_t e = cudaPeekAtLastError();
+    cudaError_t e = launch_k(mkq::gemm_w4a4_2cta_kernel<Cfg>, dim3(2 * clusters), dim3(Cfg::kThreads), Cfg::kSmem,
+                             st, 1, ma, mb, mo, ep, M, N, K);
     if (e != cudaSuccess) return cuda_fail(e, "gemm2 launch");
     return MKQ_OK;
 }
@@ -441,16 +466,16 @@ mkq_status quantize_internal(const float* x, int64_t rows, int64_t cols, int64_t
     if (vec) {
         const int g = grid_for(rows * (cols / 8), 256, sms);
         if (bits == 4) {
-            if (per_row) mkq::quantize_pack_vec_kernel<4, true><<<g, 256, 0, st>>>(x, rows, cols, ldx, scale_dev, s_val, qmin, qmax, qq, ldq);
-            else mkq::quantize_pack_vec_kernel<4, false><<<g, 256, 0, st>>>(x, rows, cols, ldx, scale_dev, s_val, qmin, qmax, qq, ldq);
+            if (per_row) launch_k(mkq::quantize_pack_vec_kernel<4, true>, dim3(g), dim3(256), 0, st, 1, x, rows, cols, ldx, scale_dev, s_val, qmin, qmax, qq, ldq);
+            else launch_k(mkq::quantize_pack_vec_kernel<4, false>, dim3(g), dim3(256), 0, st, 1, x, rows, cols, ldx, scale_dev, s_val, qmin, qmax, qq, ldq);
         } else {
-            if (per_row) mkq::quantize_pack_vec_kernel<8, true><<<g, 256, 0, st>>>(x, rows, cols, ldx, scale_dev, s_val, qmin, qmax, qq, ldq);
-            else mkq::quantize_pack_vec_kernel<8, false><<<g, 256, 0, st>>>(x, rows, cols, ldx, scale_dev, s_val, qmin, qmax, qq, ldq);
+            if (per_row) launch_k(mkq::quantize_pack_vec_kernel<8, true>, dim3(g), dim3(256), 0, st, 1, x, rows, cols, ldx, scale_dev, s_val, qmin, qmax, qq, ldq);
+            else launch_k(mkq::quantize_pack_vec_kernel<8, false>, dim3(g), dim3(256), 0, st, 1, x, rows, cols, ldx, scale_dev, s_val, qmin, qmax, qq, ldq);
         }
     } else {
         const int g = grid_for(rows * (bits == 4 ? cols / 2 : cols), 256, sms);
-        if (bits == 4) mkq::quantize_pack_any_kernel<4><<<g, 256, 0, st>>>(x, rows, cols, ldx, scale_dev, s_val, per_row, qmin, qmax, qq, ldq);
-        else mkq::quantize_pack_any_kernel<8><<<g, 256, 0, st>>>(x, rows, cols, ldx, scale_dev, s_val, per_row, qmin, qmax, qq, ldq);
+        if (bits == 4) launch_k(mkq::quantize_pack_any_kernel<4>, dim3(g), dim3(256), 0, st, 1, x, rows, cols, ldx, scale_dev, s_val, per_row, qmin, qmax, qq, ldq);
+        else launch_k(mkq::quantize_pack_any_kernel<8>, dim3(g), dim3(256), 0, st, 1, x, rows, cols, ldx, scale_dev, s_val, per_row, qmin, qmax, qq, ldq);
     }
     cudaError_t e = cudaPeekAtLastError();
     return e == cudaSuccess ? MKQ_OK : cuda_fail(e, "quantize launch");
@@ -683,7 +708,8 @@ mkq_status mkq_attention(const void* qkv, int64_t ld, int64_t batch, int64_t max
         const int64_t nitems = (int64_t)batch * heads * pairs;
         if (nitems > (1ll << 30)) return fail(MKQ_ERR_SHAPE, "too many attention work items");
         const int grid = (int)(nitems < sms ? nitems : sms);   // persistent, 1 CTA per SM
-        kern<<<grid, mkq::attnpp::kThreads, mkq::attnpp::kSmem, st>>>(mq, mkv, p, heads, pairs, (int)nitems);
+        launch_k(kern, dim3(grid), dim3(mkq::attnpp::kThreads), mkq::attnpp::kSmem, st, 1, mq, mkv, p, heads, pairs,
+                 (int)nitems);
     } else if (attn_path == 0) {
         static bool attr_set[64] = {};
         int dev = 0;
@@ -733,7 +759,7 @@ mkq_status mkq_attention(const void* qkv, int64_t ld, int64_t batch, int64_t max
     p.out = out;
     p.ldo = ldo;
     dim3 grid((unsigned)((max_seq + 63) / 64), (unsigned)heads, (unsigned)batch);
-    mkq::attn::flash_attn_kernel<<<grid, mkq::attn::kThreads, 0, st>>>(p);
+    launch_k(mkq::attn::flash_attn_kernel, grid, dim3(mkq::attn::kThreads), 0, st, 1, p);
     }
     cudaError_t e = cudaPeekAtLastError();
     return e == cudaSuccess ? MKQ_OK : cuda_fail(e, "attention launch");
@@ -765,9 +791,9 @@ mkq_status mkq_residual_layernorm(const float* x, const float* res, int64_t rows
     const int gr = grid_for(rows * 32, 256, sms);
     uint8_t* qq = static_cast<uint8_t*>(q);
     const int ci = (int)cols;
-    if (cols <= 1024) mkq::residual_ln_kernel<8><<<gr, 256, 0, st>>>(x, res, rows, ci, ld, g, b, eps, y, bits, s_q, qmin, qmax, qq, ldq);
-    else if (cols <= 2048) mkq::residual_ln_kernel<16><<<gr, 256, 0, st>>>(x, res, rows, ci, ld, g, b, eps, y, bits, s_q, qmin, qmax, qq, ldq);
-    else mkq::residual_ln_kernel<64><<<gr, 256, 0, st>>>(x, res, rows, ci, ld, g, b, eps, y, bits, s_q, qmin, qmax, qq, ldq);
+    if (cols <= 1024) launch_k(mkq::residual_ln_kernel<8>, dim3(gr), dim3(256), 0, st, 1, x, res, rows, ci, ld, g, b, eps, y, bits, s_q, qmin, qmax, qq, ldq);
+    else if (cols <= 2048) launch_k(mkq::residual_ln_kernel<16>, dim3(gr), dim3(256), 0, st, 1, x, res, rows, ci, ld, g, b, eps, y, bits, s_q, qmin, qmax, qq, ldq);
+    else launch_k(mkq::residual_ln_kernel<64>, dim3(gr), dim3(256), 0, st, 1, x, res, rows, ci, ld, g, b, eps, y, bits, s_q, qmin, qmax, qq, ldq);
     cudaError_t e = cudaPeekAtLastError();
     return e == cudaSuccess ? MKQ_OK : cuda_fail(e, "layernorm launch");
 }

@@ -386,6 +386,15 @@ __device__ __forceinline__ void sts128(uint32_t addr, const uint4& v) {
                  : "memory");
 }
 
+// Programmatic dependent launch (PDL): the next kernel on the stream may be
+// scheduled once every CTA of this grid has executed launch_dependents;
+// wait blocks until the previous grid has completed and its memory is
+// visible.  Both are no-ops when the kernel was launched without the PDL
+// attribute.  Every kernel of the layer calls wait before touching any
+// activation buffer (reads and writes), so all hazards stay ordered.
+__device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t threads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }

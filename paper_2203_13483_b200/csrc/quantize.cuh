@@ -17,6 +17,7 @@ template <int kBits, bool kPerRow>
 __global__ void __launch_bounds__(256) quantize_pack_vec_kernel(
     const float* __restrict__ x, int64_t rows, int64_t cols, int64_t ldx,
     const float* __restrict__ scale, float s_val, int qmin, int qmax, uint8_t* __restrict__ q, int64_t ldq) {
+    asm volatile("griddepcontrol.launch_dependents;\n\tgriddepcontrol.wait;" ::: "memory");   // PDL (ptx.cuh)
     const int64_t per_row = cols >> 3;
     const int64_t total = rows * per_row;
     const float s_t = (kPerRow || !scale) ? s_val : __ldg(scale);
@@ -46,6 +47,7 @@ __global__ void __launch_bounds__(256) quantize_pack_any_kernel(
     const float* __restrict__ x, int64_t rows, int64_t cols, int64_t ldx,
     const float* __restrict__ scale, float s_val, int per_row, int qmin, int qmax, uint8_t* __restrict__ q,
     int64_t ldq) {
+    asm volatile("griddepcontrol.launch_dependents;\n\tgriddepcontrol.wait;" ::: "memory");   // PDL (ptx.cuh)
     const int64_t per = kBits == 4 ? cols / 2 : cols;
     const int64_t total = rows * per;
     for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total;
