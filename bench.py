@@ -326,6 +326,10 @@ def run_ours(args):
     if rank == 0 and not args.no_table2:
         t2 = table2(torch, dev)
 
+    qat = None
+    if rank == 0:
+        qat = qat_calibration(torch, M, h_in, stream, pk)
+
     result = None
     if rank == 0:
         cpu = None if (args.no_cpu or world > 1) else cpu_baseline(sample_seqs=1)
@@ -359,12 +363,43 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "paper_comparison": cmp,
             "table2_bert_base_varlen": t2,
+            "qat_and_calibration": qat,
         }
         print(json.dumps(result))
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
     return result
+
+
+def qat_calibration(torch, M, x, stream, pk, reps=10):
+    """SURVEY §8f NEXT(3)/(4) kernels on the bench's layer input (T x hidden
+    fp32, > L2): mkq_fake_quant with every output (y, STE grad_x, STE/MSE
+    grad_s; 16 algorithmic B/element) and mkq_act_scale (the P:72 percentile
+    calibration; 3 radix passes = 12 B/element), CUDA-event timed."""
+    gy = torch.randn_like(x)
+    sc = torch.tensor([0.5558], device=x.device)
+    ws = torch.empty(int(M.lib().mkq_fake_quant_workspace_size(x.numel())), dtype=torch.uint8, device=x.device)
+    res = {}
+    with torch.cuda.stream(stream):
+        for name, fn, bpe in (
+                ("fake_quant_grad", lambda: M.mkq_fake_quant(x, sc, -8, 7, grad_y=gy, ws=ws, stream=stream), 16),
+                ("act_scale_p99.99", lambda: M.mkq_act_scale(x, 7.0, 0.9999, stream=stream), 12)):
+            for _ in range(2):
+                fn()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(reps):
+                fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            us = e0.elapsed_time(e1) / reps * 1e3
+            gbs = bpe * x.numel() / (us * 1e-6) / 1e9
+            res[name] = {"us": round(us, 1), "elements": x.numel(), "algorithmic_bytes_per_element": bpe,
+                         "gbs": round(gbs, 1), "bound": "hbm", "frac": round(gbs / pk["hbm_gbs"], 4)}
+    del gy
+    return res
 
 
 def compare_float_layers(torch, p, dev, int4_ms, args):

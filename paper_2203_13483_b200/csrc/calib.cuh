@@ -63,8 +63,17 @@ __global__ void __launch_bounds__(kThreads) hist_kernel(const float* __restrict_
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     if (vec) {
         const int64_t n4 = n >> 2;
-        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
-            const float4 v = __ldg(reinterpret_cast<const float4*>(x) + i);
+        const float4* x4 = reinterpret_cast<const float4*>(x);
+        int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+        for (; i + 3 * stride < n4; i += 4 * stride) {   // 4 x 16 B in flight per thread
+            float4 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = __ldg(x4 + i + u * stride);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) { add(v[u].x); add(v[u].y); add(v[u].z); add(v[u].w); }
+        }
+        for (; i < n4; i += stride) {
+            const float4 v = __ldg(x4 + i);
             add(v.x); add(v.y); add(v.z); add(v.w);
         }
         for (int64_t i = (n4 << 2) + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) add(x[i]);

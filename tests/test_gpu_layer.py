@@ -122,3 +122,112 @@ def test_mixed_precision_encoder_runs():
     out = host(enc(h, 2, 32, out=torch.empty_like(h)))
     assert np.isfinite(out).all()
     assert np.allclose(out.mean(-1), 0.0, atol=0.1)
+
+
+def _oracle_weights(p, bits, scales):
+    W = OL.LayerWeights(p.hidden, p.heads, p.ffn, bits,
+                        OL.prepare_weight(p.w_qkv, p.b_qkv, bits), OL.prepare_weight(p.w_o, p.b_o, bits),
+                        OL.prepare_weight(p.w_1, p.b_1, bits), OL.prepare_weight(p.w_2, p.b_2, bits),
+                        p.ln1_g, p.ln1_b, p.ln2_g, p.ln2_b)
+    W.s_qkv_in, W.s_o_in, W.s_ffn1_in, W.s_ffn2_in = (np.float32(scales[k]) for k in
+                                                      ("s_qkv_in", "s_o_in", "s_ffn1_in", "s_ffn2_in"))
+    return W
+
+
+def _end_to_end(out, h, W, seqlens):
+    T_ = OL.bert_layer(h, W, seqlens)
+    rel = np.sqrt(np.mean((out.astype(np.float64) - T_.h_out) ** 2) / np.mean(T_.h_out.astype(np.float64) ** 2))
+    return rel, T_
+
+
+def _stagewise_sampled(L, W, h, B, S, seqlens, cu_d, seqs):
+    """Stage-wise replay at full size: the GPU runs every stage of the layer
+    through the C ABI (each fed the previous GPU stage, as mkq_bert_layer
+    does); for the rows of the sampled sequences `seqs` each stage is checked
+    against the oracle stage applied to the GPU's own input rows -- bit-exact
+    for codes and integer-derived outputs, tolerance for attention / LN -- and
+    the fused layer call must equal the staged result bit for bit."""
+    bits, hidden, heads, ffn = L.bits, L.hidden, L.heads, L.ffn
+    lo, hi = model.act_range(bits)
+    gemm = M.mkq_gemm_w4a4 if bits == 4 else M.mkq_gemm_w8a8
+    pack = (lambda c: oracle.pack_int4(c)) if bits == 4 else (lambda c: c)
+    view = (lambda a: a) if bits == 4 else (lambda a: a.view(np.int8))
+    t, sc = L.t, L.scales
+    T = h.shape[0]
+    cu = np.concatenate([[0], np.cumsum(seqlens)]).astype(np.int64)
+    rows = np.concatenate([np.arange(cu[i], cu[i + 1]) for i in seqs])
+    hd = dev(h)
+    out = host(M.mkq_bert_layer(L, hd, B, S, cu_d))
+    c_in = M.mkq_quantize_pack(hd, dev(np.float32([sc["s_qkv_in"]])), bits, lo, hi)
+    codes_in = oracle.quantize(h[rows], sc["s_qkv_in"], lo, hi)
+    assert np.array_equal(view(host(c_in)[rows]), pack(codes_in))
+    qkv = gemm(c_in, t["w_qkv"], sc["s_qkv_in"], t["sw_qkv"], t["b_qkv"], mode=M.OUT_F16, K=hidden)
+    qkv_h = host(qkv)
+    ref_qkv = oracle.linear(codes_in, W.qkv.codes, W.s_qkv_in, W.qkv.s_w, W.qkv.bias, mode=oracle.OUT_F16)
+    assert np.array_equal(qkv_h[rows].view(np.uint16), ref_qkv)
+    oa_g = M.mkq_attention(qkv, heads, B, S, cu_d, mode=M.OUT_F32)
+    oa = host(oa_g)
+    ref_oa = OL.attention(qkv_h[rows].astype(np.float64), [seqlens[i] for i in seqs], heads)
+    assert np.abs(oa[rows] - ref_oa).max() < 2e-3 * max(1.0, np.abs(ref_oa).max())
+    c_oa = M.mkq_quantize_pack(oa_g, dev(np.float32([sc["s_o_in"]])), bits, lo, hi)
+    codes_oa = oracle.quantize(oa[rows], sc["s_o_in"], lo, hi)
+    assert np.array_equal(view(host(c_oa)[rows]), pack(codes_oa))
+    o_g = gemm(c_oa, t["w_o"], sc["s_o_in"], t["sw_o"], t["b_o"], mode=M.OUT_F32, K=hidden)
+    o = host(o_g)
+    assert np.array_equal(o[rows], oracle.linear(codes_oa, W.o.codes, W.s_o_in, W.o.s_w, W.o.bias))
+    h1_g, c_h1 = M.mkq_residual_layernorm(o_g, hd, t["ln1_g"], t["ln1_b"], 1e-12, bits=bits, s_q=sc["s_ffn1_in"],
+                                          qmin=lo, qmax=hi)
+    h1 = host(h1_g)
+    ref_h1 = OL.layernorm(o[rows].astype(np.float64) + h[rows], W.ln1_g, W.ln1_b)
+    assert np.abs(h1[rows] - ref_h1).max() < 2e-5 * max(1.0, np.abs(ref_h1).max())
+    codes_h1 = oracle.quantize(h1[rows], sc["s_ffn1_in"], lo, hi)
+    assert np.array_equal(view(host(c_h1)[rows]), pack(codes_h1))
+    a2 = gemm(c_h1, t["w_1"], sc["s_ffn1_in"], t["sw_1"], t["b_1"], mode=M.OUT_I4 if bits == 4 else M.OUT_I8,
+              gelu=True, s_out=sc["s_ffn2_in"], qmin=lo, qmax=hi, K=hidden, requant_table=L.table)
+    ref_a2 = oracle.linear(codes_h1, W.w1.codes, W.s_ffn1_in, W.w1.s_w, W.w1.bias,
+                           mode=oracle.OUT_I4 if bits == 4 else oracle.OUT_I8, gelu=True, s_out=W.s_ffn2_in,
+                           qmin_out=lo, qmax_out=hi)
+    assert np.array_equal(view(host(a2)[rows]), pack(ref_a2))
+    f_g = gemm(a2, t["w_2"], sc["s_ffn2_in"], t["sw_2"], t["b_2"], mode=M.OUT_F32, K=ffn)
+    f = host(f_g)
+    assert np.array_equal(f[rows], oracle.linear(ref_a2, W.w2.codes, W.s_ffn2_in, W.w2.s_w, W.w2.bias))
+    y = host(M.mkq_residual_layernorm(f_g, h1_g, t["ln2_g"], t["ln2_b"], 1e-12))
+    ref_y = OL.layernorm(f[rows].astype(np.float64) + h1[rows], W.ln2_g, W.ln2_b)
+    assert np.abs(y[rows] - ref_y).max() < 2e-5 * max(1.0, np.abs(ref_y).max())
+    assert np.array_equal(y, out)   # the fused layer runs exactly these kernels
+    # informative: end-to-end against the fully independent fp64 oracle
+    rel, T_ = _end_to_end(out[rows], h[rows], W, [seqlens[i] for i in seqs])
+    flips = int(np.sum(codes_oa != T_.codes_oa))
+    print(f"bits={bits} T={T} sampled {len(rows)} rows: end-to-end rms_rel={rel:.2e}, "
+          f"OA code flips {flips}/{codes_oa.size} (int4 amplifies near-tie flips)")
+    assert rel < 5e-2
+    d = codes_oa.astype(int) - T_.codes_oa.astype(int)
+    assert np.abs(d).max() <= 1
+
+
+@pytest.mark.parametrize("bits", [4, 8])
+def test_layer_table2_bert_base_varlen(bits):
+    """Paper Table 2 workload: one BERT-base layer (768, 12 heads,
+    3072) over a BS=16 packed batch of 440 valid tokens, in the launch
+    configuration bench.py times (small-M GEMM plan, short-sequence
+    attention, PDL), GPU-calibrated scales; stage-wise on every row."""
+    hidden, heads, ffn, S = 768, 12, 3072, 128
+    p = synth.layer_params(hidden, heads, ffn, 0)
+    L = model.build_layer(p, bits, DEV)
+    model.calibrate(L, dev(synth.hidden_states(8, S, hidden, seed=1000000)), 8, S)
+    seqlens = [int(v) for v in synth.varlen_seqlens(16, 440, S, seed=16 + 440)]
+    h = synth.hidden_states(1, 440, hidden, seed=1)
+    cu = dev(np.concatenate([[0], np.cumsum(seqlens)]).astype(np.int32))
+    _stagewise_sampled(L, _oracle_weights(p, bits, L.scales), h, 16, S, seqlens, cu, list(range(16)))
+
+
+def test_layer_bert_large_full_batch_sampled_sequence():
+    """BASELINE configs[3] at full size (BERT-large, batch 256 x seq 512 =
+    131072 tokens, bench.py's call): stage-wise on two sampled sequences
+    (every stage after attention is per row, attention per sequence)."""
+    hidden, heads, ffn, B, S = 1024, 16, 4096, 256, 512
+    p = synth.layer_params(hidden, heads, ffn, 0)
+    L = model.build_layer(p, 4, DEV)
+    model.calibrate(L, dev(synth.hidden_states(4, S, hidden, seed=1000000)), 4, S)
+    h = synth.hidden_states(B, S, hidden, seed=0)
+    _stagewise_sampled(L, _oracle_weights(p, 4, L.scales), h, B, S, [S] * B, None, [0, 173])
