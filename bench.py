@@ -329,6 +329,9 @@ def run_ours(args):
     qat = None
     if rank == 0:
         qat = qat_calibration(torch, M, h_in, stream, pk)
+    c3 = None
+    if rank == 0 and not args.no_table2:
+        c3 = c3_encoder(torch, dev)
 
     result = None
     if rank == 0:
@@ -364,12 +367,57 @@ def run_ours(args):
             "paper_comparison": cmp,
             "table2_bert_base_varlen": t2,
             "qat_and_calibration": qat,
+            "bert_base_12l_b32s128": c3,
         }
         print(json.dumps(result))
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
     return result
+
+
+def c3_encoder(torch, dev, reps=20):
+    """BASELINE.json configs[2]: BERT-base 12-layer encoder, batch 32 x seq
+    128 (4096 tokens), mixed precision per P:243 (layers 1-6 W8A8, 7-12
+    W4A4; model.bit_plan(12, 6)), plus the all-W4A4 and all-W8A8 stacks;
+    one CUDA graph per stack, mean of `reps` replays (single GPU; the
+    row-sharded multi-GPU form runs 32/g sequences per rank)."""
+    import synth
+    from paper_2203_13483_b200 import model
+    h, H, F, B, S = 768, 12, 3072, 32, 128
+    T = B * S
+    hin = torch.from_numpy(synth.hidden_states(B, S, h, seed=1)).to(dev)
+    res = {"tokens": T, "batch": B, "seq": S}
+    for name, plan in (("mixed_6w8_6w4", model.bit_plan(12, 6)), ("all_w4a4", [4] * 12), ("all_w8a8", [8] * 12)):
+        layers = []
+        for i, bits in enumerate(plan):
+            p = synth.layer_params(h, H, F, i)
+            L = model.build_layer(p, bits, dev)
+            model.calibrate(L, torch.from_numpy(synth.hidden_states(4, S, h, seed=1000000 + i)).to(dev), 4, S)
+            layers.append(L)
+        enc = model.Encoder(layers)
+        out = torch.empty_like(hin)
+        st = torch.cuda.Stream(device=dev)
+        with torch.cuda.stream(st):
+            for _ in range(2):
+                enc(hin, B, S, out=out, stream=st)
+            torch.cuda.synchronize(dev)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=st):
+                enc(hin, B, S, out=out, stream=st)
+            g.replay()
+            torch.cuda.synchronize(dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            for _ in range(reps):
+                g.replay()
+            e1.record(st)
+            torch.cuda.synchronize(dev)
+        ms = e0.elapsed_time(e1) / reps
+        res[name] = {"plan": "".join(str(b) for b in plan), "ms": round(ms, 4),
+                     "tops": round(12 * linear_ops(T, h, F) / (ms * 1e-3) / 1e12, 1),
+                     "compression_vs_fp32": round(model.compression_ratio(plan), 3)}
+    return res
 
 
 def qat_calibration(torch, M, x, stream, pk, reps=10):
