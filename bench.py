@@ -297,19 +297,46 @@ def run_ours(args):
     gemm_ms = sum(gemms.values())
     gemm_tops = ops / (gemm_ms * 1e-3) / 1e12
 
-    # ---- e2e: host buffers through the C-ABI, H2D + layer + D2H in the timed region
+    # ---- e2e: host buffers through the C-ABI, H2D + layer + D2H in the timed region.
+    # Whole sequences are independent, so the batch is processed in chunks of
+    # sequences pipelined over three streams (H2D of chunk i+1 and D2H of
+    # chunk i-1 overlap the layer on chunk i); the result is bit-identical to
+    # one call on the whole batch (checked below).
     h_pin = torch.from_numpy(h_host).pin_memory()
     o_pin = torch.empty(h_host.shape, dtype=torch.float32).pin_memory()
     e2e_steps = max(2, min(args.steps, 5))
+    nch = 8 if B % 8 == 0 else 1
+    Bc, Tc = B // nch, (B // nch) * S
+    ws_c = torch.empty(L.workspace_size(Tc), dtype=torch.uint8, device=dev)
+    s_in, s_out = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+    ev_in = [torch.cuda.Event() for _ in range(nch)]
+    ev_done = [torch.cuda.Event() for _ in range(nch)]
+
+    def e2e_step():
+        for c in range(nch):
+            rows = slice(c * Tc, (c + 1) * Tc)
+            with torch.cuda.stream(s_in):
+                if c == 0:
+                    s_in.wait_stream(s_out)          # previous step's D2H done before buffers are reused
+                h_in[rows].copy_(h_pin[rows], non_blocking=True)
+                ev_in[c].record(s_in)
+            stream.wait_event(ev_in[c])
+            M.mkq_bert_layer(L, h_in[rows], Bc, S, None, h_out=h_out[rows], ws=ws_c, stream=stream)
+            ev_done[c].record(stream)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(ev_done[c])
+                o_pin[rows].copy_(h_out[rows], non_blocking=True)
+
+    e2e_step()
     barrier()
+    e2e_same = bool(np.array_equal(o_pin.numpy(), buf["out"].cpu().numpy()))
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with torch.cuda.stream(stream):
-        e0.record(stream)
-        for _ in range(e2e_steps):
-            h_in.copy_(h_pin, non_blocking=True)
-            M.mkq_bert_layer(L, h_in, B, S, None, h_out=h_out, ws=ws, stream=stream)
-            o_pin.copy_(h_out, non_blocking=True)
-        e1.record(stream)
+    e0.record(stream)
+    s_in.wait_stream(stream)
+    for _ in range(e2e_steps):
+        e2e_step()
+    stream.wait_stream(s_out)
+    e1.record(stream)
     barrier()
     e2e_ms = e0.elapsed_time(e1) / e2e_steps
     if world > 1:
@@ -360,7 +387,9 @@ def run_ours(args):
             "roofline_by_stage": roof_all,
             "e2e": {"value": round(world * ops / (e2e_ms * 1e-3) / 1e12, 2), "unit": "TOPS",
                     "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": int(h_host.nbytes),
-                    "d2h_bytes_per_step": int(h_host.nbytes)},
+                    "d2h_bytes_per_step": int(h_host.nbytes),
+                    "pipeline": f"{nch} chunks of {Bc} sequences over H2D / compute / D2H streams",
+                    "result_equals_device_step": e2e_same},
             "gpu_launches": 8 * args.steps,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
