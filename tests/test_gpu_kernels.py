@@ -188,6 +188,56 @@ def test_gemm_worst_case_magnitudes():
     assert np.all(out == 66584576)
 
 
+@pytest.mark.parametrize("small", [0, 1])
+def test_gemm_max_k_extremes(small):
+    """K = MKQ_MAX_K = 131040 (the exactness limit of include/mkq.h): the
+    int4 accumulator holds 256 * sum = 256 * 64 * 131040 = 2147000320 < 2^31
+    for A = W = -8 (any nibble is a valid int4 code), through both GEMM plans;
+    int8 at the same K with |a w| = 128 * 127."""
+    from paper_2203_13483_b200._lib import lib
+    lib().mkq_set_small_m_mode(small)
+    try:
+        K = 131040
+        for a, w in ((-8, -8), (7, -8)):
+            A = np.full((3, K), a, np.int8)
+            W = np.full((32, K), w, np.int8)
+            out = host(_run(4, A, W, 1.0, np.ones(32, np.float32), None, mode=M.OUT_I32))
+            assert np.all(out == a * w * K)
+        A = np.full((3, K), -128, np.int8)
+        W = np.full((32, K), 127, np.int8)
+        out = host(_run(8, A, W, 1.0, np.ones(32, np.float32), None, mode=M.OUT_I32))
+        assert np.all(out == -128 * 127 * K)
+        rng = np.random.default_rng(1)
+        A, W = _codes(rng, 5, 64, K, 4)
+        assert np.array_equal(host(_run(4, A, W, 1.0, np.ones(64, np.float32), None, mode=M.OUT_I32)),
+                              oracle.gemm_i32(A, W))
+    finally:
+        lib().mkq_set_small_m_mode(-1)
+
+
+def test_degenerate_sizes():
+    """M = 0 is a no-op; the smallest legal GEMM (1 x 32 x 32); one-token
+    sequences in attention; a single LayerNorm row."""
+    rng = np.random.default_rng(2)
+    A, W = _codes(rng, 1, 32, 32, 4)
+    assert np.array_equal(host(_run(4, A, W, 1.0, np.ones(32, np.float32), None, mode=M.OUT_I32)),
+                          oracle.gemm_i32(A, W))
+    z = torch.empty((0, 16), dtype=torch.uint8, device=DEV)
+    o = M.mkq_gemm_w4a4(z, dev(oracle.pack_int4(W)), 1.0, dev(np.ones(32, np.float32)), None,
+                        mode=M.OUT_I32, out=torch.empty((0, 32), dtype=torch.int32, device=DEV), K=32)
+    assert o.shape == (0, 32)
+    # attention over three 1-token sequences: softmax of one score is 1, OA = v
+    qkv = (rng.standard_normal((3, 3 * 128)) * 0.5).astype(np.float16)
+    cu = dev(np.array([0, 1, 2, 3], np.int32))
+    oa = host(M.mkq_attention(dev(qkv), 2, 3, 1, cu, mode=M.OUT_F32))
+    assert np.allclose(oa, qkv[:, 256:].astype(np.float32), rtol=1e-3, atol=1e-3)
+    x = synth.activations(1, 768, seed=4)
+    y = host(M.mkq_residual_layernorm(dev(x), None, dev(np.ones(768, np.float32)),
+                                      dev(np.zeros(768, np.float32)), 1e-12))
+    ref = OL.layernorm(x.astype(np.float64), np.ones(768, np.float32), np.zeros(768, np.float32))
+    assert np.abs(y - ref).max() < 2e-5
+
+
 def test_gemm_zero_rows_and_strided():
     rng = np.random.default_rng(9)
     A, W = _codes(rng, 100, 256, 512, 4)
