@@ -68,6 +68,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--rep", required=True)
     ap.add_argument("--launches")
+    ap.add_argument("--last", type=int, default=24, help="count only the last N launches (the timed steps; "
+                    "tools/prof_layer.py --steps 3 = 24 launches after the setup kernels)")
     ap.add_argument("--out", required=True)
     ap.add_argument("--labels", default="quantize_in,gemm_qkv,attention,gemm_o,ln1_quant,gemm_ffn1,gemm_ffn2,ln2")
     a = ap.parse_args()
@@ -96,11 +98,11 @@ def main():
     if a.launches and os.path.exists(a.launches):
         txt = open(a.launches).read()
         start = txt.find('"ID"')
-        rows = list(csv.DictReader(io.StringIO(txt[start:])))
+        rows = [r for r in csv.DictReader(io.StringIO(txt[start:])) if r.get("Metric Name") == "gpu__time_duration.sum"]
+        if a.last > 0:
+            rows = rows[-a.last:]
         tot = {}
         for r in rows:
-            if r.get("Metric Name") != "gpu__time_duration.sum":
-                continue
             n = short(r["Kernel Name"])
             v = float(r["Metric Value"].replace(",", ""))
             unit = r.get("Metric Unit", "nsecond")
@@ -109,7 +111,8 @@ def main():
         allt = sum(sum(v) for v in tot.values())
         with open(a.out + "_launches.md", "w") as f:
             f.write(f"# Launch list ({os.path.basename(a.launches)}): "
-                    "`ncu --metrics gpu__time_duration.sum --clock-control none` over full mkq_bert_layer steps\n\n")
+                    f"`ncu --metrics gpu__time_duration.sum --clock-control none`, the last {a.last} launches "
+                    "(the timed mkq_bert_layer steps, setup kernels excluded)\n\n")
             f.write("| kernel | launches | mean us | share of step |\n|---|---|---|---|\n")
             for n, v in sorted(tot.items(), key=lambda x: -sum(x[1])):
                 f.write(f"| `{n}` | {len(v)} | {sum(v)/len(v):.1f} | {sum(v)/allt:.3f} |\n")
