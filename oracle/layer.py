@@ -98,6 +98,47 @@ def f16_round(x: np.ndarray) -> np.ndarray:
     return np.asarray(x, dtype=np.float32).astype(np.float16).astype(np.float64)
 
 
+def attention_int8(codes: np.ndarray, seqlens, heads: int, s_qkv) -> np.ndarray:
+    """NEXT(2) integer attention core (reading R19 of DESIGN.md),
+    Eq.3-5 on int8 codes of q | k | v with one per-tensor scale
+    s_qkv (Eq.1 of the QKV output, codes in [-127, 127]):
+        S_ij  = q_i . k_j                       exact integers
+        c     = fl32(fl32(s_qkv * s_qkv) * 1/8)  (1/sqrt(d_k), d_k = 64, exact)
+        d_ij  = max_j' S_ij' - S_ij              integers >= 0
+        p_ij  = rint_even(255 * exp(-c d_ij))    fp64, uint8; p = 255 at the row max
+        OA_i  = fl32(fl32(fl32(sum_j p_ij v_j) / fl32(sum_j p_ij)) * s_qkv)
+    softmax(c S) v with the probabilities held as 8-bit integers; every step
+    but the fp64 exp is exact integer arithmetic, and the final ratio is one
+    fp32 division (|sum p v| <= 255*127*128 < 2^24 for L <= 128).
+    codes: int8 [M, 3d]; returns OA fp32 [M, d]."""
+    codes = np.asarray(codes, dtype=np.int64)
+    M, three_d = codes.shape
+    d = three_d // 3
+    dk = d // heads
+    assert dk == 64
+    s = np.float32(s_qkv)
+    c = np.float32(np.float32(s * s) * np.float32(0.125))
+    out = np.zeros((M, d), dtype=np.float32)
+    r0 = 0
+    for L in seqlens:
+        rows = slice(r0, r0 + L)
+        for a in range(heads):
+            cols = slice(a * dk, (a + 1) * dk)
+            q = codes[rows, 0 * d:1 * d][:, cols]
+            k = codes[rows, 1 * d:2 * d][:, cols]
+            v = codes[rows, 2 * d:3 * d][:, cols]
+            S = q @ k.T                                          # exact int64
+            dd = S.max(axis=1, keepdims=True) - S                # >= 0
+            p = np.rint(255.0 * np.exp(-(np.float64(c) * dd.astype(np.float64)))).astype(np.int64)
+            num = p @ v                                          # exact
+            den = p.sum(axis=1, keepdims=True)
+            y = (num.astype(np.float32) / den.astype(np.float32)).astype(np.float32)
+            out[rows, cols] = (y * s).astype(np.float32)
+        r0 += L
+    assert r0 == M
+    return out
+
+
 def attention(qkv: np.ndarray, seqlens, heads: int) -> np.ndarray:
     """Eq.3-5 per sequence and head, fp64.
 

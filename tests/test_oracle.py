@@ -394,3 +394,71 @@ def test_layer_oracle_small_runs_and_is_consistent():
     assert T.codes_ffn2_in.min() >= -8 and T.codes_ffn2_in.max() <= 7
     # the quantized layer tracks the fp32 layer (QAT's premise): loose check
     assert np.isfinite(T.h_out).all()
+
+
+# ---------------------------------------------------------------- NEXT(2) integer attention (R19)
+def _codes_qkv(rng, L, heads=1, lim=127):
+    return rng.integers(-lim, lim + 1, (L, 3 * 64 * heads)).astype(np.int8)
+
+
+def test_int_attention_single_token_is_v():
+    """L = 1: softmax of one score is 1 -> p = 255, OA = s * v exactly."""
+    rng = np.random.default_rng(0)
+    c = _codes_qkv(rng, 1, 2)
+    s = np.float32(0.031)
+    oa = OL.attention_int8(c, [1], 2, s)
+    assert np.array_equal(oa, (c[:, 256:].astype(np.float32) * s).astype(np.float32))
+
+
+def test_int_attention_equal_keys_is_mean_and_dominant_key_is_one_hot():
+    rng = np.random.default_rng(1)
+    s = np.float32(0.05)
+    L = 17
+    c = _codes_qkv(rng, L)
+    c[:, 64:128] = c[0, 64:128]                  # identical keys -> all p = 255
+    oa = OL.attention_int8(c, [L], 1, s)
+    v = c[:, 128:].astype(np.int64)
+    mean = (np.float32(255 * v.sum(0)) / np.float32(255 * L)).astype(np.float32)
+    assert np.array_equal(oa[0], (mean * s).astype(np.float32))
+    # one key aligned with every query, the rest zero: c*d = 0.0025*127*127*64/8 ~ 322 >> ln(254)
+    c2 = np.zeros((L, 192), np.int8)
+    c2[:, :64] = 127
+    c2[5, 64:128] = 127
+    c2[:, 128:] = _codes_qkv(rng, L)[:, 128:]
+    oa2 = OL.attention_int8(c2, [L], 1, s)
+    assert np.array_equal(oa2, np.tile((c2[5, 128:].astype(np.float32) * s).astype(np.float32), (L, 1)))
+
+
+def test_int_attention_close_to_float_softmax():
+    """Against the fp64 softmax of c*S on the dequantized v: each p_ij is
+    255 e_ij rounded (error <= 1/2) and sum p >= 255, so
+    |OA_int - OA| <= s max|v| L / 255."""
+    rng = np.random.default_rng(2)
+    s = np.float32(0.02)
+    for L in (3, 40, 128):
+        c = _codes_qkv(rng, L)
+        oa = OL.attention_int8(c, [L], 1, s).astype(np.float64)
+        q, k, v = (c[:, i * 64:(i + 1) * 64].astype(np.float64) for i in range(3))
+        cc = float(np.float32(np.float32(s * s) * np.float32(0.125)))
+        ref = OL.softmax(cc * (q @ k.T)) @ (v * float(s))
+        bound = float(s) * np.abs(v).max() * L / 255
+        assert np.abs(oa - ref).max() <= bound
+
+
+def test_int_attention_bruteforce_tiny():
+    """Per-element loop with Python ints and math.exp (independent of numpy's
+    vectorized path) on a tiny case."""
+    import math
+    rng = np.random.default_rng(3)
+    s = np.float32(0.04)
+    L = 5
+    c = _codes_qkv(rng, L, lim=20)
+    oa = OL.attention_int8(c, [L], 1, s)
+    cc = float(np.float32(np.float32(s * s) * np.float32(0.125)))
+    for i in range(L):
+        S = [sum(int(c[i, t]) * int(c[j, 64 + t]) for t in range(64)) for j in range(L)]
+        p = [int(round(255 * math.exp(-cc * (max(S) - S[j])))) for j in range(L)]   # no exact ties here
+        for t in range(64):
+            num = sum(p[j] * int(c[j, 128 + t]) for j in range(L))
+            y = np.float32(np.float32(num) / np.float32(sum(p)))
+            assert oa[i, t] == np.float32(y * s)
