@@ -189,6 +189,22 @@ MKQ_API mkq_status mkq_attention(const void *qkv, int64_t ld_qkv_elems, int64_t 
                          int out_mode, float s_out, int qmin, int qmax, void *out,
                          int64_t ldo_bytes, void *stream);
 
+/* integer attention core for short sequences (reading
+ * R19; Eq.3-5).  qkv [device] int8 codes [tokens, 3*heads*64] =
+ * [q | k | v] (Eq.1 of the QKV GEMM output with the per-tensor scale s_qkv,
+ * codes in [-127, 127]; the MKQ_OUT_I8 epilogue of mkq_gemm_*), row stride
+ * ld_qkv_bytes.  Per sequence and head:
+ *   S_ij = q_i . k_j (exact int32);  c = fl32(fl32(s_qkv*s_qkv) / 8);
+ *   p_ij = rint_even(255 * exp(-c * (max_j S_ij - S_ij)))  (fp64 exp, uint8);
+ *   OA_i = fl32(fl32(fl32(sum_j p_ij v_j) / fl32(sum_j p_ij)) * s_qkv).
+ * Every step but the fp64 exp is exact; results equal the oracle bit for bit
+ * unless 255*exp(.) falls within an ulp of a half-integer.  max_seq <= 128,
+ * head_dim 64; cu_seqlens / out_mode / s_out / qmin / qmax as mkq_attention. */
+MKQ_API mkq_status mkq_attention_i8(const void *qkv, int64_t ld_qkv_bytes, int64_t batch, int64_t max_seq,
+                                    const int32_t *cu_seqlens, int64_t tokens, int heads, int head_dim,
+                                    float s_qkv, int out_mode, float s_out, int qmin, int qmax, void *out,
+                                    int64_t ldo_bytes, void *stream);
+
 /* §8a-a8 glue: y = LayerNorm(x + res) * g + b (post-LN, eps, fp32; R9), and
  * optionally (bits = 4 or 8, else 0) the fused Eq.1 quantize of y with the
  * per-tensor scale s_q into q (packed like mkq_quantize_pack).

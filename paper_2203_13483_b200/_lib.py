@@ -34,6 +34,7 @@ SIGNATURES = {
     "mkq_requant_table_size": (SZ, []),
     "mkq_requant_table": (I32, [I32, F32, I32, I32, P, SZ, P]),
     "mkq_attention": (I32, [P, I64, I64, I64, P, I64, I32, I32, I32, F32, I32, I32, P, I64, P]),
+    "mkq_attention_i8": (I32, [P, I64, I64, I64, P, I64, I32, I32, F32, I32, F32, I32, I32, P, I64, P]),
     "mkq_residual_layernorm": (I32, [P, P, I64, I64, I64, P, P, F32, P, I32, F32, I32, I32, P, I64, P]),
     "mkq_interleave_blocks": (I32, [P, P, I64, I64, I64, I64, P]),
     "mkq_fake_quant_workspace_size": (SZ, [I64]),

@@ -20,6 +20,7 @@
 #include "attention.cuh"
 #include "attention_sm100.cuh"
 #include "attention_pp_sm100.cuh"
+#include "attention_i8.cuh"
 #include "gemm_sm100.cuh"
 #include "gemm2_sm100.cuh"
 #include "requant.cuh"
@@ -776,6 +777,55 @@ mkq_status mkq_attention(const void* qkv, int64_t ld, int64_t batch, int64_t max
     }
     cudaError_t e = cudaPeekAtLastError();
     return e == cudaSuccess ? MKQ_OK : cuda_fail(e, "attention launch");
+}
+
+mkq_status mkq_attention_i8(const void* qkv, int64_t ld, int64_t batch, int64_t max_seq, const int32_t* cu,
+                            int64_t tokens, int heads, int head_dim, float s_qkv, int out_mode, float s_out, int qmin,
+                            int qmax, void* out, int64_t ldo, void* stream) {
+    if (batch < 0 || max_seq < 0 || tokens < 0) return fail(MKQ_ERR_SHAPE, "negative dimension");
+    if (batch == 0 || tokens == 0) return MKQ_OK;
+    if (!qkv || !out) return fail(MKQ_ERR_NULL, "qkv and out are required");
+    if (head_dim != 64) return fail(MKQ_ERR_SHAPE, "head_dim must be 64");
+    if (heads <= 0 || heads > 65535) return fail(MKQ_ERR_SHAPE, "heads out of range");
+    if (max_seq <= 0 || max_seq > mkq::attn8::kMaxL) return fail(MKQ_ERR_SHAPE, "max_seq must be in [1, 128]");
+    if (batch > 65535) return fail(MKQ_ERR_SHAPE, "batch must be <= 65535");
+    if (!cu && tokens != batch * max_seq) return fail(MKQ_ERR_SHAPE, "tokens != batch*max_seq without cu_seqlens");
+    const int64_t hidden = (int64_t)heads * 64;
+    if (ld < 3 * hidden) return fail(MKQ_ERR_SHAPE, "ld_qkv smaller than 3*hidden bytes");
+    if (!aligned16(qkv) || ld % 16) return fail(MKQ_ERR_ALIGN, "qkv rows must be 16-byte aligned");
+    int64_t orow;
+    if (out_mode == MKQ_OUT_F32) orow = 4 * hidden;
+    else if (out_mode == MKQ_OUT_I4) orow = hidden / 2;
+    else if (out_mode == MKQ_OUT_I8) orow = hidden;
+    else return fail(MKQ_ERR_RANGE, "attention out_mode must be F32, I4 or I8");
+    if (ldo < orow) return fail(MKQ_ERR_SHAPE, "ldo smaller than a row");
+    if (!aligned16(out) || ldo % 16) return fail(MKQ_ERR_ALIGN, "out rows must be 16-byte aligned");
+    if (!finite_pos(s_qkv)) return fail(MKQ_ERR_SCALE, "s_qkv must be > 0 and finite");
+    if (out_mode != MKQ_OUT_F32) {
+        if (!finite_pos(s_out)) return fail(MKQ_ERR_SCALE, "s_out must be > 0 and finite");
+        if (!code_range_ok(out_mode == MKQ_OUT_I4 ? 4 : 8, qmin, qmax)) return fail(MKQ_ERR_RANGE, "qmin/qmax");
+    }
+    mkq_status s = check_device();
+    if (s != MKQ_OK) return s;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    PdlScope pdl_scope(tokens);
+    mkq::attn8::Params p;
+    p.qkv = static_cast<const int8_t*>(qkv);
+    p.ld = ld;
+    p.cu = cu;
+    p.seq = (int)max_seq;
+    p.hidden = (int)hidden;
+    p.s = s_qkv;
+    p.out_mode = out_mode;
+    p.s_out = s_out;
+    p.qmin = qmin;
+    p.qmax = qmax;
+    p.out = out;
+    p.ldo = ldo;
+    launch_k(mkq::attn8::attn_i8_kernel, dim3((unsigned)heads, (unsigned)batch), dim3(mkq::attn8::kThreads), 0, st, 1,
+             p);
+    cudaError_t e = cudaPeekAtLastError();
+    return e == cudaSuccess ? MKQ_OK : cuda_fail(e, "attention_i8 launch");
 }
 
 mkq_status mkq_residual_layernorm(const float* x, const float* res, int64_t rows, int64_t cols, int64_t ld,

@@ -15,7 +15,7 @@ from ._lib import (OUT_BF16, OUT_F16, OUT_F32, OUT_I32, OUT_I4, OUT_I8, MkqEpilo
 
 __all__ = ["mkq_requant_table", "mkq_quantize_pack", "mkq_absmax_scale", "mkq_gemm_w4a4", "mkq_gemm_w8a8",
            "mkq_attention", "mkq_residual_layernorm", "mkq_bert_layer", "mkq_interleave_blocks", "mkq_fake_quant",
-           "mkq_act_scale", "out_dtype_bytes",
+           "mkq_act_scale", "mkq_attention_i8", "out_dtype_bytes",
            "OUT_F32", "OUT_BF16", "OUT_I32", "OUT_I4", "OUT_I8", "OUT_F16"]
 
 
@@ -198,6 +198,21 @@ def mkq_attention(qkv: torch.Tensor, heads: int, batch: int, max_seq: int,
     check("mkq_attention", lib().mkq_attention(
         _ptr(qkv), qkv.stride(0), batch, max_seq, _ptr(cu_seqlens), T, heads, 64, mode, float(s_out), qmin, qmax,
         _ptr(out), _row_bytes(out), _stream(stream)))
+    return out
+
+
+def mkq_attention_i8(qkv: torch.Tensor, heads: int, batch: int, max_seq: int, s_qkv: float,
+                     cu_seqlens: Optional[torch.Tensor] = None, mode: int = OUT_F32, s_out: float = 1.0,
+                     qmin: int = -8, qmax: int = 7, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """NEXT(2) integer attention core (R19) on int8 qkv codes [tokens, 3*hidden]."""
+    T = qkv.shape[0]
+    hidden = heads * 64
+    if out is None:
+        dt, nb = out_dtype_bytes(mode)
+        out = torch.empty((T, int(hidden * nb) if mode == OUT_I4 else hidden), dtype=dt, device=qkv.device)
+    check("mkq_attention_i8", lib().mkq_attention_i8(
+        _ptr(qkv), _row_bytes(qkv), batch, max_seq, _ptr(cu_seqlens), T, heads, 64, float(s_qkv), mode,
+        float(s_out), qmin, qmax, _ptr(out), _row_bytes(out), _stream(stream)))
     return out
 
 
