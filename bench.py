@@ -543,11 +543,11 @@ def table2(torch, dev, reps=50):
     h, H, F, S = 768, 12, 3072, 128
     p = synth.layer_params(h, H, F, 0)
     layers = {}
-    for bits in (4, 8):
+    for key, bits, ia in (("int4", 4, False), ("int8", 8, False), ("int4_int_attention", 4, True)):
         L = model.build_layer(p, bits, dev)
         hc = torch.from_numpy(synth.hidden_states(8, S, h, seed=1000000)).to(dev)
-        model.calibrate(L, hc, 8, S)
-        layers[bits] = L
+        model.calibrate(L, hc, 8, S, int_attention=ia)
+        layers[key] = L
     W = {k: torch.from_numpy(getattr(p, k)).to(dev) for k in
          ("w_qkv", "b_qkv", "w_o", "b_o", "w_1", "b_1", "w_2", "b_2", "ln1_g", "ln1_b", "ln2_g", "ln2_b")}
     torch.backends.cuda.matmul.allow_tf32 = False
@@ -557,8 +557,8 @@ def table2(torch, dev, reps=50):
         cu = torch.tensor(np.concatenate([[0], np.cumsum(lens)]).astype(np.int32), device=dev)
         hin = torch.from_numpy(synth.hidden_states(1, valid, h, seed=1)).to(dev)
         res = {"bs": bs, "valid_tokens": valid}
-        for bits in (4, 8):
-            L = layers[bits]
+        for key in ("int4", "int8", "int4_int_attention"):
+            L = layers[key]
             out = torch.empty_like(hin)
             ws = torch.empty(L.workspace_size(valid), dtype=torch.uint8, device=dev)
             st = torch.cuda.Stream(device=dev)
@@ -577,7 +577,7 @@ def table2(torch, dev, reps=50):
                 g.replay()
             e1.record()
             torch.cuda.synchronize(dev)
-            res[f"int{bits}_us"] = round(e0.elapsed_time(e1) / reps * 1e3, 1)
+            res[f"{key}_us"] = round(e0.elapsed_time(e1) / reps * 1e3, 1)
         # fp32 torch layer on the padded batch (key padding mask)
         x = torch.zeros(bs, S, h, device=dev)
         mask = torch.zeros(bs, S, dtype=torch.bool, device=dev)

@@ -264,7 +264,9 @@ MKQ_API mkq_status mkq_act_scale(const float *x, int64_t n, double p, float l_ma
  * One quantized post-LN BERT encoder layer (§8a rows a1-a8 composed):
  *   c   = Q(h; s_qkv_in)                                   a1
  *   qkv = f16( Linear_{W^{QKV}}(c) )                        a2-a4
- *   OA  = Attention(qkv) -> Q(.; s_o_in)                    a8 (fused quantize)
+ *         (int_attention: Q(Linear(c); s_attn), int8 codes)
+ *   OA  = Attention(qkv) -> Q(.; s_o_in)                    a8 (fused quantize;
+ *         int_attention: mkq_attention_i8)
  *   o   = Linear_{W^A}(.) (+b^A), fp32                      a2-a4
  *   h1  = LN1(o + h) -> fp32 and Q(h1; s_ffn1_in)           a8 + a1 fused
  *   a2  = Q(GELU(Linear_{W^1}(.)); s_ffn2_in)               a2-a6 (fused)
@@ -287,6 +289,11 @@ typedef struct {
     /* optional [device] mkq_requant_table(1, s_ffn2_in, qmin, qmax) for the
      * FFN1 epilogue (NULL = direct evaluation; identical results) */
     const void *ffn1_requant_table;
+    /* NEXT(2): 1 = integer attention core (R19): the QKV epilogue emits int8
+     * codes [-127, 127] with the per-tensor scale s_attn and attention runs
+     * mkq_attention_i8 (max_seq <= 128); 0 = fp16 q|k|v (R10). */
+    int32_t int_attention;
+    float s_attn;
 } mkq_layer;
 
 /* Workspace bytes for `tokens` rows (intermediates of one layer). */

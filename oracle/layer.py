@@ -76,6 +76,9 @@ class LayerWeights:
     s_o_in: np.float32 = np.float32(1)
     s_ffn1_in: np.float32 = np.float32(1)
     s_ffn2_in: np.float32 = np.float32(1)
+    # NEXT(2) integer attention core (R19): scale of the int8 q|k|v codes;
+    # None = fp16 attention operands (R10)
+    s_attn: object = None
 
 
 def layernorm(x: np.ndarray, g: np.ndarray, b: np.ndarray, eps: float = LN_EPS) -> np.ndarray:
@@ -186,9 +189,14 @@ def bert_layer(h: np.ndarray, W: LayerWeights, seqlens) -> LayerTrace:
     lo, hi = act_range(W.bits)
     h = np.asarray(h, dtype=np.float32)
     T.codes_in = quantize(h, W.s_qkv_in, lo, hi)
-    qkv16 = linear(T.codes_in, W.qkv.codes, W.s_qkv_in, W.qkv.s_w, W.qkv.bias, mode=OUT_F16)
-    T.qkv = qkv16.view(np.float16).astype(np.float64)
-    T.oa = attention(T.qkv, seqlens, W.heads).astype(np.float32)
+    if W.s_attn is not None:   # NEXT(2): Eq.1 of the QKV output to int8, integer attention (R19)
+        T.qkv = linear(T.codes_in, W.qkv.codes, W.s_qkv_in, W.qkv.s_w, W.qkv.bias, mode=OUT_I8,
+                       s_out=W.s_attn, qmin_out=-127, qmax_out=127)
+        T.oa = attention_int8(T.qkv, seqlens, W.heads, W.s_attn)
+    else:
+        qkv16 = linear(T.codes_in, W.qkv.codes, W.s_qkv_in, W.qkv.s_w, W.qkv.bias, mode=OUT_F16)
+        T.qkv = qkv16.view(np.float16).astype(np.float64)
+        T.oa = attention(T.qkv, seqlens, W.heads).astype(np.float32)
     T.codes_oa = quantize(T.oa, W.s_o_in, lo, hi)
     T.o = linear(T.codes_oa, W.o.codes, W.s_o_in, W.o.s_w, W.o.bias, mode=OUT_F32)
     T.h1 = layernorm(T.o.astype(np.float64) + h, W.ln1_g, W.ln1_b).astype(np.float32)
@@ -201,18 +209,26 @@ def bert_layer(h: np.ndarray, W: LayerWeights, seqlens) -> LayerTrace:
     return T
 
 
-def calibrate(h_calib: np.ndarray, W: LayerWeights, seqlens) -> LayerWeights:
-    """Sequential calibration of the four static activation scales
+def calibrate(h_calib: np.ndarray, W: LayerWeights, seqlens, int_attention: bool = False) -> LayerWeights:
+    """Sequential calibration of the static activation scales
     (P:72 'top 0.01% largest value', P:121 calibration step; R6/O-S):
     each scale is set from the layer's own activations on a calibration
-    batch, in pipeline order, using the scales already fixed upstream."""
+    batch, in pipeline order, using the scales already fixed upstream
+    (int_attention: also s_attn = p99.99(|q|k|v|) / 127, R19)."""
     lo, hi = act_range(W.bits)
     h = np.asarray(h_calib, dtype=np.float32)
     W.s_qkv_in = act_scale(h, hi)
     codes = quantize(h, W.s_qkv_in, lo, hi)
-    qkv = linear(codes, W.qkv.codes, W.s_qkv_in, W.qkv.s_w, W.qkv.bias,
-                 mode=OUT_F16).view(np.float16).astype(np.float64)
-    oa = attention(qkv, seqlens, W.heads).astype(np.float32)
+    if int_attention:
+        qkv32 = linear(codes, W.qkv.codes, W.s_qkv_in, W.qkv.s_w, W.qkv.bias, mode=OUT_F32)
+        W.s_attn = act_scale(qkv32, 127)
+        qkv8 = linear(codes, W.qkv.codes, W.s_qkv_in, W.qkv.s_w, W.qkv.bias, mode=OUT_I8, s_out=W.s_attn,
+                      qmin_out=-127, qmax_out=127)
+        oa = attention_int8(qkv8, seqlens, W.heads, W.s_attn)
+    else:
+        qkv = linear(codes, W.qkv.codes, W.s_qkv_in, W.qkv.s_w, W.qkv.bias,
+                     mode=OUT_F16).view(np.float16).astype(np.float64)
+        oa = attention(qkv, seqlens, W.heads).astype(np.float32)
     W.s_o_in = act_scale(oa, hi)
     o = linear(quantize(oa, W.s_o_in, lo, hi), W.o.codes, W.s_o_in, W.o.s_w, W.o.bias)
     h1 = layernorm(o.astype(np.float64) + h, W.ln1_g, W.ln1_b).astype(np.float32)

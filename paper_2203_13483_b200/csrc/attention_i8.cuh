@@ -9,7 +9,7 @@
 //                                                  exact u8 x s8 -> s32 MMA, one fp32 ratio
 // fused with the Eq.1 quantize of OA for the W^A GEMM (or fp32 out).
 //
-// One CTA (4 warps) per (head, sequence): q, k and v^T of the sequence are
+// One CTA (4 warps) per (head, sequence, 64-query tile): q, k and v^T of the sequence are
 // staged in shared memory (row pitches chosen so every fragment load is
 // bank-conflict-free), each warp owns 16-query row blocks; S stays in
 // registers, the probabilities go through a per-warp shared-memory tile to
@@ -57,25 +57,41 @@ __device__ __forceinline__ void mma_u8s8(int (&c)[4], uint32_t a0, uint32_t a1, 
 }
 __device__ __forceinline__ uint32_t lds32(const uint8_t* p) { return *reinterpret_cast<const uint32_t*>(p); }
 
-// p = rint_even(255 exp(-c d)) in fp64 (R19); 0 once 255 e^{-x} < 0.5 surely
-__device__ __forceinline__ uint32_t prob_code(double c, int d) {
-    const double x = __dmul_rn(c, (double)d);   // exact: 24-bit c times d < 2^22
-    if (x > 6.3) return 0u;                      // 255 e^-6.3 = 0.47 < 0.5
-    return (uint32_t)rint(__dmul_rn(255.0, exp(-x)));
+// p = rint_even(255 exp(-c d)), defined in fp64 (R19); 0 once 255 e^-x < 0.5.
+// Fast path in fp32: x32 = RN(c d) (relative error <= 2^-24 x <= 3.8e-7 in
+// e^-x), expf (<= 2 ulp = 2.4e-7) and the product (6e-8) put e32 within
+// 255 * 6.8e-7 = 1.7e-4 of the fp64 value 255 e^-x, so rint(e32) is the fp64
+// decision whenever e32 is more than 2.5e-4 away from a half-integer;
+// otherwise (about 0.05% of the values) the fp64 definition decides.
+__device__ __noinline__ uint32_t prob_code_f64(double c64, int d) {   // one out-of-line copy (i-cache)
+    return (uint32_t)rint(__dmul_rn(255.0, exp(-__dmul_rn(c64, (double)d))));
 }
+__device__ __forceinline__ uint32_t prob_code(float c32, double c64, int d) {
+    const float x = __fmul_rn(c32, (float)d);   // (float)d exact: d < 2^22
+    if (x > 6.3f) return 0u;                     // 255 e^-6.3 = 0.47 < 0.5
+    const float e = __fmul_rn(255.0f, expf(-x));
+    const float r = rintf(e);
+    if (fabsf(fabsf(__fsub_rn(e, r)) - 0.5f) > 2.5e-4f) return (uint32_t)r;
+    return prob_code_f64(c64, d);
+}
+
+constexpr int kPS = kMaxL + 4;   // staged S row pitch (int32 words)
+constexpr int kSmem = 2 * kMaxL * kPQ + kD * kPV + 4 * 16 * kPV + 4 * 16 * kPS * 4;
 
 __global__ void __launch_bounds__(kThreads) attn_i8_kernel(const Params p) {
     asm volatile("griddepcontrol.launch_dependents;\n\tgriddepcontrol.wait;" ::: "memory");   // PDL (ptx.cuh)
-    __shared__ __align__(16) uint8_t Qs[kMaxL * kPQ];
-    __shared__ __align__(16) uint8_t Ks[kMaxL * kPQ];
-    __shared__ __align__(16) uint8_t Vt[kD * kPV];
-    __shared__ __align__(16) uint8_t Ps[4][16 * kPV];
+    extern __shared__ __align__(16) uint8_t smem[];
+    uint8_t* Qs = smem;
+    uint8_t* Ks = Qs + kMaxL * kPQ;
+    uint8_t* Vt = Ks + kMaxL * kPQ;
+    uint8_t* Pall = Vt + kD * kPV;
+    int* Sall = reinterpret_cast<int*>(Pall + 4 * 16 * kPV);
     const int head = blockIdx.x, b = blockIdx.y;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int g = lane >> 2, t = lane & 3;
     const int start = p.cu ? p.cu[b] : b * p.seq;
     const int L = p.cu ? (p.cu[b + 1] - start) : p.seq;
-    if (L <= 0) return;
+    if (L <= 0 || (int)blockIdx.z * 64 >= L) return;
     const int Lk = (L + 31) & ~31;   // keys padded to the MMA K of P . V
     // ---- stage q, k (row-major) and v^T; zero the padding rows / columns
     for (int i = tid; i < Lk * 4; i += kThreads) {
@@ -95,10 +111,14 @@ __global__ void __launch_bounds__(kThreads) attn_i8_kernel(const Params p) {
     }
     __syncthreads();
     const float s = p.s;
-    const double cc = (double)__fmul_rn(__fmul_rn(s, s), 0.125f);
+    const float c32 = __fmul_rn(__fmul_rn(s, s), 0.125f);
+    const double cc = (double)c32;
     const int nt = (L + 7) >> 3;   // key n-tiles of S
-    uint8_t* P = Ps[warp];
-    for (int rb = warp; rb * 16 < L; rb += 4) {
+    uint8_t* P = Pall + warp * 16 * kPV;
+    int* Sw = Sall + warp * 16 * kPS;
+    const QuantRcp Qo = quant_rcp(p.out_mode ? p.s_out : 1.0f, p.qmin, p.qmax);
+    // CTA z = 64-query tile (4 warps x 16 rows), like the fp16 flash kernel
+    for (int rb = blockIdx.z * 4 + warp; rb * 16 < L && rb < blockIdx.z * 4 + 4; rb += 4) {
         const int r0 = rb * 16;
         // ---- S = q k^T (exact int32)
         int acc[16][4];
@@ -116,43 +136,36 @@ __global__ void __launch_bounds__(kThreads) attn_i8_kernel(const Params p) {
                 }
             }
         }
-        // ---- row maxima over the valid keys (rows g and g+8 of the block)
-        int m0 = INT_MIN, m1 = INT_MIN;
+        // ---- stage S (int32) in the warp's tile; the per-element softmax work
+        // runs in rolled loops below (small code: the fully unrolled form
+        // was instruction-fetch bound)
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
             if (j < nt) {
-                const int col = 8 * j + 2 * t;
-                if (col < L) { m0 = max(m0, acc[j][0]); m1 = max(m1, acc[j][2]); }
-                if (col + 1 < L) { m0 = max(m0, acc[j][1]); m1 = max(m1, acc[j][3]); }
+                *reinterpret_cast<int2*>(Sw + g * kPS + 8 * j + 2 * t) = make_int2(acc[j][0], acc[j][1]);
+                *reinterpret_cast<int2*>(Sw + (g + 8) * kPS + 8 * j + 2 * t) = make_int2(acc[j][2], acc[j][3]);
             }
         }
-#pragma unroll
-        for (int o = 1; o <= 2; o <<= 1) {
-            m0 = max(m0, __shfl_xor_sync(0xffffffffu, m0, o));
-            m1 = max(m1, __shfl_xor_sync(0xffffffffu, m1, o));
+        __syncwarp();
+        // lane -> (row lane & 15, column half lane >> 4)
+        const int rr = lane & 15, hh = lane >> 4;
+        const int half = (L + 1) >> 1, c0 = hh * half, c1 = min(L, c0 + half);
+        const int* Srow = Sw + rr * kPS;
+        int mx = INT_MIN;
+#pragma unroll 4
+        for (int c = c0; c < c1; ++c) mx = max(mx, Srow[c]);
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+        int den = 0;
+        uint8_t* Prow = P + rr * kPV;
+#pragma unroll 2
+        for (int c = c0; c < c1; ++c) {
+            const uint32_t pc = prob_code(c32, cc, mx - Srow[c]);
+            den += (int)pc;
+            Prow[c] = (uint8_t)pc;
         }
-        // ---- 8-bit probabilities -> P tile (A operand of P . V), row sums
-        int den0 = 0, den1 = 0;
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            if (8 * j < Lk) {
-                const int col = 8 * j + 2 * t;
-                uint32_t p00 = 0, p01 = 0, p10 = 0, p11 = 0;
-                if (j < nt) {
-                    if (col < L) { p00 = prob_code(cc, m0 - acc[j][0]); p10 = prob_code(cc, m1 - acc[j][2]); }
-                    if (col + 1 < L) { p01 = prob_code(cc, m0 - acc[j][1]); p11 = prob_code(cc, m1 - acc[j][3]); }
-                }
-                den0 += (int)(p00 + p01);
-                den1 += (int)(p10 + p11);
-                *reinterpret_cast<uint16_t*>(P + g * kPV + col) = (uint16_t)(p00 | (p01 << 8));
-                *reinterpret_cast<uint16_t*>(P + (g + 8) * kPV + col) = (uint16_t)(p10 | (p11 << 8));
-            }
-        }
-#pragma unroll
-        for (int o = 1; o <= 2; o <<= 1) {
-            den0 += __shfl_xor_sync(0xffffffffu, den0, o);
-            den1 += __shfl_xor_sync(0xffffffffu, den1, o);
-        }
+        for (int c = L + hh; c < Lk; c += 2) Prow[c] = 0;   // padded keys
+        den += __shfl_xor_sync(0xffffffffu, den, 16);
+        const int den0 = __shfl_sync(0xffffffffu, den, g), den1 = __shfl_sync(0xffffffffu, den, g + 8);
         __syncwarp();
         // ---- num = P . V (exact int32), 8 d-tiles of 8
         int o_acc[8][4];
@@ -183,9 +196,11 @@ __global__ void __launch_bounds__(kThreads) attn_i8_kernel(const Params p) {
                 const float y1 = __fmul_rn(__fdiv_rn((float)o_acc[n][2 * hrow + 1], fd), s);
                 if (p.out_mode == 0) {
                     *reinterpret_cast<float2*>(orow + (int64_t)col * 4) = make_float2(y0, y1);
-                } else {
-                    const int q0 = quant_code(y0, p.s_out, p.qmin, p.qmax);
-                    const int q1 = quant_code(y1, p.s_out, p.qmin, p.qmax);
+                } else {   // Eq.1 via the reciprocal with the exact fallback near ties (epilogue.cuh)
+                    const float yy[2] = {y0, y1};
+                    int qq[2];
+                    quant_group_rcp(yy, Qo, qq);
+                    const int q0 = qq[0], q1 = qq[1];
                     if (p.out_mode == 3)
                         orow[col >> 1] = (uint8_t)((q0 & 0xF) | ((q1 & 0xF) << 4));
                     else

@@ -822,8 +822,18 @@ mkq_status mkq_attention_i8(const void* qkv, int64_t ld, int64_t batch, int64_t 
     p.qmax = qmax;
     p.out = out;
     p.ldo = ldo;
-    launch_k(mkq::attn8::attn_i8_kernel, dim3((unsigned)heads, (unsigned)batch), dim3(mkq::attn8::kThreads), 0, st, 1,
-             p);
+    static bool attr_set[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!attr_set[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(mkq::attn8::attn_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             mkq::attn8::kSmem);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(attn_i8)");
+        attr_set[dev] = true;
+    }
+    launch_k(mkq::attn8::attn_i8_kernel, dim3((unsigned)heads, (unsigned)batch, (unsigned)((max_seq + 63) / 64)),
+             dim3(mkq::attn8::kThreads),
+             mkq::attn8::kSmem, st, 1, p);
     cudaError_t e = cudaPeekAtLastError();
     return e == cudaSuccess ? MKQ_OK : cuda_fail(e, "attention_i8 launch");
 }
@@ -1000,6 +1010,9 @@ mkq_status mkq_bert_layer(const mkq_layer* L, const float* h_in, int64_t batch, 
     if (!finite_pos(L->s_qkv_in) || !finite_pos(L->s_o_in) || !finite_pos(L->s_ffn1_in) || !finite_pos(L->s_ffn2_in))
         return fail(MKQ_ERR_SCALE, "activation scales must be > 0 and finite");
     if (!cu && T != batch * max_seq) return fail(MKQ_ERR_SHAPE, "tokens != batch*max_seq without cu_seqlens");
+    if (L->int_attention != 0 && L->int_attention != 1) return fail(MKQ_ERR_RANGE, "int_attention must be 0 or 1");
+    if (L->int_attention && !finite_pos(L->s_attn)) return fail(MKQ_ERR_SCALE, "s_attn must be > 0 and finite");
+    if (L->int_attention && max_seq > 128) return fail(MKQ_ERR_SHAPE, "int_attention needs max_seq <= 128");
     const LayerWs W = layer_ws(L, T);
     if (ws_bytes < W.total) return fail(MKQ_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes, W.total);
     if (!aligned16(ws)) return fail(MKQ_ERR_ALIGN, "workspace must be 16-byte aligned");
@@ -1033,12 +1046,21 @@ mkq_status mkq_bert_layer(const mkq_layer* L, const float* h_in, int64_t batch, 
     // a1: quantize the layer input (per-tensor static scale, by value)
     MKQ_TRY(quantize_internal(h_in, T, h, h, nullptr, L->s_qkv_in, 0, bits, qlo, qhi, codes_in, cbh, sms, st));
     // a2-a4: QKV projection -> fp16 q|k|v (R10)
-    mkq_epilogue e_f16{MKQ_OUT_F16, 0, 1.0f, 0, 0, nullptr};
-    MKQ_TRY(gemm(codes_in, cbh, L->w_qkv, cbh, T, 3 * h, h, L->s_qkv_in, L->sw_qkv, L->b_qkv, &e_f16, qkv,
-                 3 * h * 2, nullptr, 0, stream));
-    // a8: attention core, fused quantize of OA with s_o_in
-    MKQ_TRY(mkq_attention(qkv, 3 * h, batch, max_seq, cu, T, L->heads, 64, bits == 4 ? MKQ_OUT_I4 : MKQ_OUT_I8,
-                          L->s_o_in, qlo, qhi, codes_oa, cbh, stream));
+    if (L->int_attention) {
+        // NEXT(2): int8 q|k|v codes (Eq.1, s_attn, [-127,127]) -> integer attention core (R19)
+        mkq_epilogue e_i8{MKQ_OUT_I8, 0, L->s_attn, -127, 127, nullptr};
+        MKQ_TRY(gemm(codes_in, cbh, L->w_qkv, cbh, T, 3 * h, h, L->s_qkv_in, L->sw_qkv, L->b_qkv, &e_i8, qkv,
+                     3 * h, nullptr, 0, stream));
+        MKQ_TRY(mkq_attention_i8(qkv, 3 * h, batch, max_seq, cu, T, L->heads, 64, L->s_attn,
+                                 bits == 4 ? MKQ_OUT_I4 : MKQ_OUT_I8, L->s_o_in, qlo, qhi, codes_oa, cbh, stream));
+    } else {
+        mkq_epilogue e_f16{MKQ_OUT_F16, 0, 1.0f, 0, 0, nullptr};
+        MKQ_TRY(gemm(codes_in, cbh, L->w_qkv, cbh, T, 3 * h, h, L->s_qkv_in, L->sw_qkv, L->b_qkv, &e_f16, qkv,
+                     3 * h * 2, nullptr, 0, stream));
+        // a8: attention core, fused quantize of OA with s_o_in
+        MKQ_TRY(mkq_attention(qkv, 3 * h, batch, max_seq, cu, T, L->heads, 64, bits == 4 ? MKQ_OUT_I4 : MKQ_OUT_I8,
+                              L->s_o_in, qlo, qhi, codes_oa, cbh, stream));
+    }
     // W^A projection (+ b^A) -> fp32
     mkq_epilogue e_f32{MKQ_OUT_F32, 0, 1.0f, 0, 0, nullptr};
     MKQ_TRY(gemm(codes_oa, cbh, L->w_o, cbh, T, h, h, L->s_o_in, L->sw_o, L->b_o, &e_f32, o, h * 4, nullptr, 0,

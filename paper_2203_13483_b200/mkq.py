@@ -250,9 +250,14 @@ class QLayer:
 
     def __init__(self, hidden: int, heads: int, ffn: int, bits: int, tensors: dict, scales: dict,
                  ln_eps: float = 1e-12, use_table: bool = True):
+        """scales: s_qkv_in, s_o_in, s_ffn1_in, s_ffn2_in, and optionally s_attn
+        (present and > 0 = NEXT(2) integer attention core)."""
         self.hidden, self.heads, self.ffn, self.bits = hidden, heads, ffn, bits
         self.t = {k: tensors[k].contiguous() for k in self.FIELDS}
         self.scales = {k: float(scales[k]) for k in ("s_qkv_in", "s_o_in", "s_ffn1_in", "s_ffn2_in")}
+        if scales.get("s_attn"):
+            self.scales["s_attn"] = float(scales["s_attn"])
+        self.int_attention = "s_attn" in self.scales
         self.ln_eps = ln_eps
         lo, hi = (-8, 7) if bits == 4 else (-128, 127)
         dev = self.t["w_qkv"].device
@@ -260,7 +265,8 @@ class QLayer:
         self.c = MkqLayer(hidden, heads, ffn, bits, *[self.t[k].data_ptr() for k in self.FIELDS],
                           self.scales["s_qkv_in"], self.scales["s_o_in"], self.scales["s_ffn1_in"],
                           self.scales["s_ffn2_in"], float(ln_eps),
-                          None if self.table is None else self.table.data_ptr())
+                          None if self.table is None else self.table.data_ptr(),
+                          int(self.int_attention), float(self.scales.get("s_attn", 0.0)))
 
     def workspace_size(self, tokens: int) -> int:
         return int(lib().mkq_bert_layer_workspace_size(ctypes.byref(self.c), tokens))

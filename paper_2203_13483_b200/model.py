@@ -55,10 +55,12 @@ def build_layer(params, bits: int, device="cuda", scales: Optional[Dict[str, flo
 
 
 def calibrate(layer: M.QLayer, h: torch.Tensor, batch: int, max_seq: int,
-              cu_seqlens: Optional[torch.Tensor] = None) -> Dict[str, float]:
-    """Sequential calibration of the four static activation scales on a
+              cu_seqlens: Optional[torch.Tensor] = None, int_attention: bool = False) -> Dict[str, float]:
+    """Sequential calibration of the static activation scales on a
     calibration batch, each quantization point in pipeline
-    order with the scales already fixed upstream; returns and installs them."""
+    order with the scales already fixed upstream; returns and installs them.
+    int_attention: also calibrate s_attn (p99.99 of |q|k|v| / 127) and run
+    the NEXT(2) integer attention core (R19)."""
     bits, hd, F = layer.bits, layer.hidden, layer.ffn
     lo, hi = act_range(bits)
     t = layer.t
@@ -66,8 +68,15 @@ def calibrate(layer: M.QLayer, h: torch.Tensor, batch: int, max_seq: int,
     s = {}
     s["s_qkv_in"] = act_scale(h, hi)
     c = M.mkq_quantize_pack(h, torch.tensor([s["s_qkv_in"]], device=h.device), bits, lo, hi)
-    qkv = gemm(c, t["w_qkv"], s["s_qkv_in"], t["sw_qkv"], t["b_qkv"], mode=M.OUT_F16, K=hd)
-    oa = M.mkq_attention(qkv, layer.heads, batch, max_seq, cu_seqlens, mode=M.OUT_F32)
+    if int_attention:
+        qkv32 = gemm(c, t["w_qkv"], s["s_qkv_in"], t["sw_qkv"], t["b_qkv"], mode=M.OUT_F32, K=hd)
+        s["s_attn"] = act_scale(qkv32, 127)
+        qkv8 = gemm(c, t["w_qkv"], s["s_qkv_in"], t["sw_qkv"], t["b_qkv"], mode=M.OUT_I8, s_out=s["s_attn"],
+                    qmin=-127, qmax=127, K=hd, requant_table=False)
+        oa = M.mkq_attention_i8(qkv8, layer.heads, batch, max_seq, s["s_attn"], cu_seqlens, mode=M.OUT_F32)
+    else:
+        qkv = gemm(c, t["w_qkv"], s["s_qkv_in"], t["sw_qkv"], t["b_qkv"], mode=M.OUT_F16, K=hd)
+        oa = M.mkq_attention(qkv, layer.heads, batch, max_seq, cu_seqlens, mode=M.OUT_F32)
     s["s_o_in"] = act_scale(oa, hi)
     c = M.mkq_quantize_pack(oa, torch.tensor([s["s_o_in"]], device=h.device), bits, lo, hi)
     o = gemm(c, t["w_o"], s["s_o_in"], t["sw_o"], t["b_o"], mode=M.OUT_F32, K=hd)

@@ -231,3 +231,40 @@ def test_layer_bert_large_full_batch_sampled_sequence():
     model.calibrate(L, dev(synth.hidden_states(4, S, hidden, seed=1000000)), 4, S)
     h = synth.hidden_states(B, S, hidden, seed=0)
     _stagewise_sampled(L, _oracle_weights(p, 4, L.scales), h, B, S, [S] * B, None, [0, 173])
+
+
+@pytest.mark.parametrize("bits", [4, 8])
+@pytest.mark.parametrize("cfg", ["small", "table2"])
+def test_layer_integer_attention(bits, cfg):
+    """NEXT(2): the layer with the integer attention core (R19).  The QKV
+    codes and the attention output are bit-exact against the oracle (no
+    float attention left), so the layer output differs from the fp64 oracle
+    only through LayerNorm rounding."""
+    if cfg == "small":
+        hidden, heads, ffn, S, seqlens = 256, 4, 1024, 128, [1, 17, 100, 5]
+    else:
+        hidden, heads, ffn, S = 768, 12, 3072, 128
+        seqlens = [int(v) for v in synth.varlen_seqlens(16, 440, S, seed=16 + 440)]
+    p = synth.layer_params(hidden, heads, ffn, 0)
+    L = model.build_layer(p, bits, DEV)
+    model.calibrate(L, dev(synth.hidden_states(8, S, hidden, seed=1000000)), 8, S, int_attention=True)
+    assert L.int_attention and L.scales["s_attn"] > 0
+    W = _oracle_weights(p, bits, L.scales)
+    W.s_attn = np.float32(L.scales["s_attn"])
+    T = sum(seqlens)
+    h = synth.hidden_states(1, T, hidden, seed=2)
+    cu = dev(np.concatenate([[0], np.cumsum(seqlens)]).astype(np.int32))
+    out = host(M.mkq_bert_layer(L, dev(h), len(seqlens), S, cu))
+    T_ = OL.bert_layer(h, W, seqlens)
+    # stage-wise: int8 q|k|v codes and the attention output through the C ABI
+    lo, hi = model.act_range(bits)
+    gemm = M.mkq_gemm_w4a4 if bits == 4 else M.mkq_gemm_w8a8
+    c_in = M.mkq_quantize_pack(dev(h), dev(np.float32([L.scales["s_qkv_in"]])), bits, lo, hi)
+    qkv8 = gemm(c_in, L.t["w_qkv"], L.scales["s_qkv_in"], L.t["sw_qkv"], L.t["b_qkv"], mode=M.OUT_I8,
+                s_out=L.scales["s_attn"], qmin=-127, qmax=127, K=hidden, requant_table=False)
+    assert np.array_equal(host(qkv8).view(np.int8), T_.qkv)
+    oa = host(M.mkq_attention_i8(qkv8, heads, len(seqlens), S, L.scales["s_attn"], cu, mode=M.OUT_F32))
+    assert np.array_equal(oa, T_.oa)
+    rel = np.sqrt(np.mean((out.astype(np.float64) - T_.h_out) ** 2) / np.mean(T_.h_out.astype(np.float64) ** 2))
+    print(f"int attention bits={bits} {cfg}: end-to-end rms_rel={rel:.2e}")
+    assert rel < 5e-3
