@@ -157,11 +157,34 @@ __global__ void __launch_bounds__(kThreads) attn_i8_kernel(const Params p) {
         mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
         int den = 0;
         uint8_t* Prow = P + rr * kPV;
-#pragma unroll 2
-        for (int c = c0; c < c1; ++c) {
-            const uint32_t pc = prob_code(c32, cc, mx - Srow[c]);
-            den += (int)pc;
-            Prow[c] = (uint8_t)pc;
+        // 4 independent elements per step, branch-free fast path (__expf:
+        // <= 2 + 1.17x ulp = 9 ulp for x <= 6.3, so e32 is within 3.9e-4 of
+        // 255 e^-x; any element within 5e-4 of a half-integer takes the fp64
+        // definition, about 0.1% of them)
+        for (int c = c0; c < c1; c += 4) {
+            uint32_t pc[4];
+            bool near = false;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int d = (c + i < c1) ? mx - Srow[c + i] : 1 << 21;
+                const float x = __fmul_rn(c32, (float)d);
+                const float e = __fmul_rn(255.0f, __expf(-x));
+                const float r = rintf(e);
+                near |= (x <= 6.3f) && !(fabsf(fabsf(__fsub_rn(e, r)) - 0.5f) > 5e-4f);
+                pc[i] = x > 6.3f ? 0u : (uint32_t)r;
+            }
+            if (near) {
+#pragma unroll 1
+                for (int i = 0; i < 4; ++i)
+                    if (c + i < c1) pc[i] = prob_code(c32, cc, mx - Srow[c + i]);
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                if (c + i < c1) {
+                    den += (int)pc[i];
+                    Prow[c + i] = (uint8_t)pc[i];
+                }
+            }
         }
         for (int c = L + hh; c < Lk; c += 2) Prow[c] = 0;   // padded keys
         den += __shfl_xor_sync(0xffffffffu, den, 16);
