@@ -291,7 +291,6 @@ size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct SmallPlan {
     bool use = false;
-    int bn = 64;
     int splits = 1;
     int64_t tiles = 0;
 };
@@ -343,12 +342,10 @@ SmallPlan plan_small(int64_t M, int64_t N, int64_t K, int sms) {
     const int mode = small_m_mode();
     if (mode == 0) return p;
     const int64_t mt = (M + 127) / 128;
-    const int64_t t64 = mt * ((N + 63) / 64), t128 = mt * ((N + 127) / 128);
+    const int64_t t64 = mt * ((N + 63) / 64);
     // (128 x 128 tiles measured slower than the 2-CTA 256 x 256 path at
     // Table-2 sizes: t64 > sms goes to the large-tile paths)
-    (void)t128;
     if (t64 <= sms || mode == 1) {
-        p.bn = 64;
         p.tiles = t64;
     } else {
         return p;
@@ -418,10 +415,6 @@ mkq_status gemm_common(bool int4, const void* a, int64_t lda, const void* w, int
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const SmallPlan sp = plan_small(M, N, K, sms);
     if (sp.use) {
-        if (sp.bn == 128) {
-            if (int4) return launch_gemm<mkq::GemmCfg<128, true>, true>(a, lda, w, ldw, (int)M, (int)N, (int)K, ep, sms, st, sp.splits);
-            return launch_gemm<mkq::GemmCfg<128, false>, true>(a, lda, w, ldw, (int)M, (int)N, (int)K, ep, sms, st, sp.splits);
-        }
         if (int4) return launch_gemm<mkq::GemmCfg<64, true>, true>(a, lda, w, ldw, (int)M, (int)N, (int)K, ep, sms, st, sp.splits);
         return launch_gemm<mkq::GemmCfg<64, false>, true>(a, lda, w, ldw, (int)M, (int)N, (int)K, ep, sms, st, sp.splits);
     }
