@@ -226,12 +226,12 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < S8; ++i) {
-            ptx::mbar_init(&full8[i], kInt4 ? 128 : 1);
+            ptx::mbar_init(&full8[i], kInt4 ? (kCl ? 32 : 128) : 1);
             ptx::mbar_init(&empty8[i], 1);
         }
         for (int i = 0; i < SP; ++i) {
             ptx::mbar_init(&fullP[i], 1);
-            ptx::mbar_init(&emptyP[i], 128);
+            ptx::mbar_init(&emptyP[i], kCl ? 32 : 128);
         }
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(&tfull[i], 1);
@@ -376,6 +376,45 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
         const int u = threadIdx.x - 256;
         constexpr int kChunks = (BM + BN) * (Cfg::BK / 32);   // 16-byte packed chunks / stage
         static_assert(kChunks % 128 == 0, "chunk split");
+        if constexpr (kCl && kInt4) {
+            // Small-M plan (one unit per CTA, SP == S8 == 4 == unpack warps):
+            // unpack warp w owns ring slot w and unpacks whole stages w, w+4, ...,
+            // so four stages are expanded in parallel instead of four warps
+            // sharing each stage in turn (stage spacing was 0.45 us for int4
+            // against 0.32 us of TMA for int8, tools/trace_small.py).
+            static_assert(Cfg::SP == 4 && Cfg::S8 == 4, "warp-per-stage unpack");
+            const int w = warp - 8;
+            int kb0, kb1;
+            k_range(blockIdx.x, kb0, kb1);
+            for (int j = w; kb0 + j < kb1; j += 4) {
+                const uint32_t ph = (uint32_t)(j >> 2) & 1u;
+                ptx::mbar_wait(&fullP[w], ph);
+                ptx::mbar_wait(&empty8[w], ph ^ 1);
+                const uint8_t* src = ringP + w * Cfg::kStageP;
+                uint8_t* dst = ring8 + w * Cfg::kStage8;
+#pragma unroll 6
+                for (int i = 0; i < kChunks / 32; ++i) {
+                    const int id = lane + 32 * i;
+                    const int r = id >> 2, c = id & 3;
+                    const uint4 p = *reinterpret_cast<const uint4*>(src + r * 64 + c * 16);
+                    uint4 lo, hi;
+                    lo.x = (p.x << 4) & 0xF0F0F0F0u; hi.x = p.x & 0xF0F0F0F0u;
+                    lo.y = (p.y << 4) & 0xF0F0F0F0u; hi.y = p.y & 0xF0F0F0F0u;
+                    lo.z = (p.z << 4) & 0xF0F0F0F0u; hi.z = p.z & 0xF0F0F0F0u;
+                    lo.w = (p.w << 4) & 0xF0F0F0F0u; hi.w = p.w & 0xF0F0F0F0u;
+                    const int r7 = r & 7;
+                    uint8_t* drow = dst + r * 128;
+                    *reinterpret_cast<uint4*>(drow + (((2 * c) ^ r7) << 4)) = lo;
+                    *reinterpret_cast<uint4*>(drow + (((2 * c + 1) ^ r7) << 4)) = hi;
+                }
+                ptx::fence_proxy_async_smem();
+                ptx::mbar_arrive(&full8[w]);
+                ptx::mbar_arrive(&emptyP[w]);
+            }
+            // tail: this slot's last MMA commit has landed
+            const int jl = (kb1 - kb0 - 1 - w) >= 0 ? ((kb1 - kb0 - 1 - w) / 4) * 4 + w : -1;
+            if (jl >= 0) ptx::mbar_wait(&empty8[w], (uint32_t)((jl >> 2) & 1));
+        } else {
         int sp = 0, s8 = 0;
         uint32_t php = 0, ph8 = 0;
         for (int unit = blockIdx.x; unit < num_tiles; unit += gridDim.x) {
@@ -411,6 +450,7 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
         for (int i = 0; i < S8; ++i) {   // tail: the MMA's last commits on empty8 have landed
             ptx::mbar_wait(&empty8[s8], ph8 ^ 1);
             if (++s8 == S8) { s8 = 0; ph8 ^= 1; }
+        }
         }
     }
 
