@@ -168,7 +168,8 @@ MKQ_API size_t mkq_gemm_workspace_size(int64_t M, int64_t N, int64_t K);
 
 /* Diagnostics / tests: GEMM tile plan for small M.  -1 = heuristic (default;
  * also the MKQ_SMALL_M environment variable), 0 = never the small-M plan,
- * 1 = always.  Results are identical in every mode. */
+ * 1 = always the tcgen05 cluster split-K plan, 2 = always the mma.sync
+ * small-M kernel.  Results are identical in every mode. */
 MKQ_API void mkq_set_small_m_mode(int mode);
 
 /* ------------------------------------------------------------------------

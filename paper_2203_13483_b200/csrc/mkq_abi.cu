@@ -23,6 +23,7 @@
 #include "attention_i8.cuh"
 #include "gemm_sm100.cuh"
 #include "gemm2_sm100.cuh"
+#include "gemm_mma_small.cuh"
 #include "requant.cuh"
 #include "layernorm.cuh"
 #include "quantize.cuh"
@@ -413,6 +414,35 @@ mkq_status gemm_common(bool int4, const void* a, int64_t lda, const void* w, int
     ep.out = out;
     ep.ldo_bytes = ldo;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    // mma.sync small-M kernel: latency-first (mode 2 forces it; heuristic:
+    // set by MKQ_MMA_SMALL_M rows, default 0 = off until measured)
+    static const int mma_rows = [] { const char* e = getenv("MKQ_MMA_SMALL_M"); return e ? atoi(e) : 0; }();
+    if (small_m_mode() == 2 || (small_m_mode() == -1 && M <= mma_rows)) {
+        PdlScope pdl_scope_m(M);
+        static bool attr[2][64] = {};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        const int ii = int4 ? 1 : 0;
+        if (!attr[ii][dev]) {
+            cudaError_t e = int4 ? cudaFuncSetAttribute(mkq::gsm::gemm_mma_small_kernel<true>,
+                                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                        mkq::gsm::Cfg<true>::kSmem)
+                                 : cudaFuncSetAttribute(mkq::gsm::gemm_mma_small_kernel<false>,
+                                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                        mkq::gsm::Cfg<false>::kSmem);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(gemm_mma_small)");
+            attr[ii][dev] = true;
+        }
+        const dim3 grid((unsigned)((N + mkq::gsm::BN - 1) / mkq::gsm::BN), (unsigned)((M + mkq::gsm::BM - 1) / mkq::gsm::BM));
+        cudaError_t e = int4 ? launch_k(mkq::gsm::gemm_mma_small_kernel<true>, grid, dim3(mkq::gsm::kThreads),
+                                        mkq::gsm::Cfg<true>::kSmem, st, 1, static_cast<const uint8_t*>(a), lda,
+                                        static_cast<const uint8_t*>(w), ldw, ep, (int)M, (int)N, (int)K)
+                             : launch_k(mkq::gsm::gemm_mma_small_kernel<false>, grid, dim3(mkq::gsm::kThreads),
+                                        mkq::gsm::Cfg<false>::kSmem, st, 1, static_cast<const uint8_t*>(a), lda,
+                                        static_cast<const uint8_t*>(w), ldw, ep, (int)M, (int)N, (int)K);
+        if (e != cudaSuccess) return cuda_fail(e, "gemm_mma_small launch");
+        return MKQ_OK;
+    }
     const SmallPlan sp = plan_small(M, N, K, sms);
     if (sp.use) {
         if (int4) return launch_gemm<mkq::GemmCfg<64, true>, true>(a, lda, w, ldw, (int)M, (int)N, (int)K, ep, sms, st, sp.splits);
@@ -565,7 +595,7 @@ mkq_status mkq_gemm_w8a8(const void* a, int64_t lda, const void* w, int64_t ldw,
     return gemm_common(false, a, lda, w, ldw, M, N, K, s_a, s_w, bias, epi, out, ldo, ws, ws_bytes, stream);
 }
 
-void mkq_set_small_m_mode(int mode) { g_small_mode.store(mode < 0 ? -1 : (mode ? 1 : 0)); }
+void mkq_set_small_m_mode(int mode) { g_small_mode.store(mode < 0 ? -1 : (mode > 2 ? 2 : mode)); }
 
 size_t mkq_gemm_workspace_size(int64_t, int64_t, int64_t) { return 0; }
 

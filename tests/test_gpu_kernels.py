@@ -85,7 +85,7 @@ SHAPES = [(1, 32, 32), (7, 64, 96), (128, 768, 768), (129, 256, 160), (300, 512,
           (1000, 3072, 768)]
 
 
-@pytest.fixture(params=[-1, 0, 1], ids=["plan-auto", "plan-large", "plan-small"])
+@pytest.fixture(params=[-1, 0, 1, 2], ids=["plan-auto", "plan-large", "plan-small", "plan-mma"])
 def small_mode(request):
     """GEMM tile plan: heuristic, never / always the small-M split-K plan."""
     from paper_2203_13483_b200._lib import lib
@@ -108,9 +108,10 @@ def test_gemm_raw_i32_bitexact(bits, Mm, N, K, small_mode):
 @pytest.mark.parametrize("bits", [4, 8])
 @pytest.mark.parametrize("Mm,N,K", [(440, 768, 3072), (440, 2304, 768), (440, 3072, 768), (440, 768, 768),
                                      (1, 768, 3072), (130, 64, 4096), (2298, 768, 768)])
-def test_gemm_small_m_split_k(bits, Mm, N, K):
+@pytest.mark.parametrize("plan", [1, 2])
+def test_gemm_small_m_split_k(bits, Mm, N, K, plan):
     from paper_2203_13483_b200._lib import lib
-    lib().mkq_set_small_m_mode(1)
+    lib().mkq_set_small_m_mode(plan)
     try:
         rng = np.random.default_rng(Mm + N + K + bits)
         A, W = _codes(rng, Mm, N, K, bits)
@@ -188,7 +189,7 @@ def test_gemm_worst_case_magnitudes():
     assert np.all(out == 66584576)
 
 
-@pytest.mark.parametrize("small", [0, 1])
+@pytest.mark.parametrize("small", [0, 1, 2])
 def test_gemm_max_k_extremes(small):
     """K = MKQ_MAX_K = 131040 (the exactness limit of include/mkq.h): the
     int4 accumulator holds 256 * sum = 256 * 64 * 131040 = 2147000320 < 2^31
