@@ -18,7 +18,11 @@ __device__ __forceinline__ float warp_sum(float v) {
     return v;
 }
 
-template <int VPL>   // float4 vectors per lane (cols <= 128*VPL)
+// VPL: float4 vectors per lane (cols <= 128*VPL).  kPre: gamma/beta issued
+// together with the row loads (one memory round trip instead of two): used
+// for small row counts (latency-bound); at large row counts the extra
+// registers cost occupancy and bandwidth (measured 304 -> 439 us).
+template <int VPL, bool kPre = false>
 __global__ void __launch_bounds__(256) residual_ln_kernel(
     const float* __restrict__ x, const float* __restrict__ res, int64_t rows, int cols, int64_t ld,
     const float* __restrict__ g, const float* __restrict__ b, float eps, float* __restrict__ y,
@@ -31,8 +35,18 @@ __global__ void __launch_bounds__(256) residual_ln_kernel(
     for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += warps) {
         const float4* xr = reinterpret_cast<const float4*>(x + r * ld);
         const float4* rr = res ? reinterpret_cast<const float4*>(res + r * ld) : nullptr;
-        float4 v[VPL];
+        float4 v[VPL], gg[kPre ? VPL : 1], bb[kPre ? VPL : 1];
         float s = 0.f;
+        if constexpr (kPre) {
+#pragma unroll
+            for (int i = 0; i < VPL; ++i) {
+                const int c = lane + 32 * i;
+                if (c < nv) {
+                    gg[i] = __ldg(reinterpret_cast<const float4*>(g) + c);
+                    bb[i] = __ldg(reinterpret_cast<const float4*>(b) + c);
+                }
+            }
+        }
 #pragma unroll
         for (int i = 0; i < VPL; ++i) {
             const int c = lane + 32 * i;
@@ -64,13 +78,13 @@ __global__ void __launch_bounds__(256) residual_ln_kernel(
         for (int i = 0; i < VPL; ++i) {
             const int c = lane + 32 * i;
             if (c < nv) {
-                const float4 gg = __ldg(reinterpret_cast<const float4*>(g) + c);
-                const float4 bb = __ldg(reinterpret_cast<const float4*>(b) + c);
+                const float4 g4 = kPre ? gg[kPre ? i : 0] : __ldg(reinterpret_cast<const float4*>(g) + c);
+                const float4 b4 = kPre ? bb[kPre ? i : 0] : __ldg(reinterpret_cast<const float4*>(b) + c);
                 float4 o;
-                o.x = (v[i].x - mean) * rstd * gg.x + bb.x;
-                o.y = (v[i].y - mean) * rstd * gg.y + bb.y;
-                o.z = (v[i].z - mean) * rstd * gg.z + bb.z;
-                o.w = (v[i].w - mean) * rstd * gg.w + bb.w;
+                o.x = (v[i].x - mean) * rstd * g4.x + b4.x;
+                o.y = (v[i].y - mean) * rstd * g4.y + b4.y;
+                o.z = (v[i].z - mean) * rstd * g4.z + b4.z;
+                o.w = (v[i].w - mean) * rstd * g4.w + b4.w;
                 yr[c] = o;
                 if (bits) {
                     const float ov[4] = {o.x, o.y, o.z, o.w};

@@ -888,7 +888,8 @@ mkq_status mkq_residual_layernorm(const float* x, const float* res, int64_t rows
     PdlScope pdl_scope(rows);
     uint8_t* qq = static_cast<uint8_t*>(q);
     const int ci = (int)cols;
-    if (cols <= 1024) launch_k(mkq::residual_ln_kernel<8>, dim3(gr), dim3(256), 0, st, 1, x, res, rows, ci, ld, g, b, eps, y, bits, s_q, qmin, qmax, qq, ldq);
+    if (cols <= 1024 && rows <= 16384) launch_k(mkq::residual_ln_kernel<8, true>, dim3(gr), dim3(256), 0, st, 1, x, res, rows, ci, ld, g, b, eps, y, bits, s_q, qmin, qmax, qq, ldq);
+    else if (cols <= 1024) launch_k(mkq::residual_ln_kernel<8>, dim3(gr), dim3(256), 0, st, 1, x, res, rows, ci, ld, g, b, eps, y, bits, s_q, qmin, qmax, qq, ldq);
     else if (cols <= 2048) launch_k(mkq::residual_ln_kernel<16>, dim3(gr), dim3(256), 0, st, 1, x, res, rows, ci, ld, g, b, eps, y, bits, s_q, qmin, qmax, qq, ldq);
     else launch_k(mkq::residual_ln_kernel<64>, dim3(gr), dim3(256), 0, st, 1, x, res, rows, ci, ld, g, b, eps, y, bits, s_q, qmin, qmax, qq, ldq);
     cudaError_t e = cudaPeekAtLastError();
