@@ -54,6 +54,7 @@ def main():
         w = torch.randint(0, 256, (max(dims), K // 2), generator=g, device="cuda", dtype=torch.uint8)
         wf = torch.randn(max(dims), K, device="cuda")
         wb = wf.bfloat16()
+        wi_all = torch.randint(-128, 128, (max(dims), K), device="cuda", dtype=torch.int8)
         for N in dims:
             s_w = torch.full((N,), 1e-3, device="cuda")
             bias = torch.zeros(N, device="cuda")
@@ -65,6 +66,14 @@ def main():
                 f32 = timeit(lambda: torch.matmul(xf, wf[:N].t()), a.reps)
                 xb = xf.bfloat16()
                 bf16 = timeit(lambda: torch.matmul(xb, wb[:N].t()), a.reps)
+                i8 = None
+                try:   # cuBLASLt int8 (torch._int_mm): the practical int8 tensor ceiling
+                    if Mm > 16:
+                        xi = torch.randint(-128, 128, (Mm, K), device="cuda", dtype=torch.int8)
+                        wi = wi_all[:N].t()
+                        i8 = timeit(lambda: torch._int_mm(xi, wi), a.reps)
+                except Exception:
+                    i8 = None
                 ops = 2.0 * Mm * N * K
                 byts = Mm * K / 2 + N * K / 2 + 4 * Mm * N + 8 * N
                 t_tc, t_hbm = ops / (int8_peak * 1e12) * 1e6, byts / (hbm * 1e9) * 1e6
@@ -74,18 +83,19 @@ def main():
                              "gbs": round(byts / ours / 1e3, 1), "bound": bound,
                              "roofline_frac": round(max(t_tc, t_hbm) / ours, 4),
                              "cublas_f32_us": round(f32, 2), "cublas_bf16_us": round(bf16, 2),
+                             "cublaslt_int8_us": None if i8 is None else round(i8, 2),
                              "speedup_vs_f32": round(f32 / ours, 2), "speedup_vs_bf16": round(bf16 / ours, 2)})
                 del x, out, xf, xb
         print(f"K={K} done", flush=True)
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     with open(os.path.join(ROOT, "gpurun_out", "gemm_sweep.json"), "w") as f:
         json.dump({"peaks": pk, "rows": rows}, f)
-    lines = ["| M | N | K | ours us | TOPS | frac int8 peak | GB/s | bound | roofline frac | cuBLAS fp32 us | cuBLAS bf16 us | x fp32 | x bf16 |",
-             "|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
+    lines = ["| M | N | K | ours us | TOPS | frac int8 peak | GB/s | bound | roofline frac | cuBLAS fp32 us | cuBLAS bf16 us | cuBLASLt int8 us | x fp32 | x bf16 |",
+             "|---|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
     for r in rows:
         lines.append("| " + " | ".join(str(r[k]) for k in ("M", "N", "K", "us", "tops", "frac_int8_peak", "gbs", "bound",
                                                            "roofline_frac", "cublas_f32_us", "cublas_bf16_us",
-                                                           "speedup_vs_f32", "speedup_vs_bf16")) + " |")
+                                                           "cublaslt_int8_us", "speedup_vs_f32", "speedup_vs_bf16")) + " |")
     with open(os.path.join(ROOT, "gpurun_out", "gemm_sweep.md"), "w") as f:
         f.write("\n".join(lines) + "\n")
 
