@@ -93,21 +93,37 @@ __global__ void __launch_bounds__(kThreads) attn_i8_kernel(const Params p) {
     const int L = p.cu ? (p.cu[b + 1] - start) : p.seq;
     if (L <= 0 || (int)blockIdx.z * 64 >= L) return;
     const int Lk = (L + 31) & ~31;   // keys padded to the MMA K of P . V
-    // ---- stage q, k (row-major) and v^T; zero the padding rows / columns
+    // ---- stage q, k (row-major); zero the padding rows
     for (int i = tid; i < Lk * 4; i += kThreads) {
         const int r = i >> 2, c = i & 3;
-        uint4 q = make_uint4(0, 0, 0, 0), k = q, v = q;
+        uint4 q = make_uint4(0, 0, 0, 0), k = q;
         if (r < L) {
             const int8_t* row = p.qkv + (int64_t)(start + r) * p.ld + head * kD + c * 16;
             q = *reinterpret_cast<const uint4*>(row);
             k = *reinterpret_cast<const uint4*>(row + p.hidden);
-            v = *reinterpret_cast<const uint4*>(row + 2 * p.hidden);
         }
         *reinterpret_cast<uint4*>(Qs + r * kPQ + c * 16) = q;
         *reinterpret_cast<uint4*>(Ks + r * kPQ + c * 16) = k;
-        const uint32_t vw[4] = {v.x, v.y, v.z, v.w};
+    }
+    // v^T: each thread transposes 4 keys x 4 d-values in registers (PRMT) and
+    // writes four 32-bit words (byte stores were the LSU hot spot)
+    for (int i = tid; i < (Lk >> 2) * 16; i += kThreads) {
+        const int kq = i >> 4, dq = i & 15;
+        uint32_t rw[4];
 #pragma unroll
-        for (int e = 0; e < 16; ++e) Vt[(c * 16 + e) * kPV + r] = (uint8_t)(vw[e >> 2] >> (8 * (e & 3)));
+        for (int u = 0; u < 4; ++u) {
+            const int r = 4 * kq + u;
+            rw[u] = r < L ? *reinterpret_cast<const uint32_t*>(p.qkv + (int64_t)(start + r) * p.ld + 2 * p.hidden +
+                                                                head * kD + 4 * dq)
+                          : 0u;
+        }
+        const uint32_t t0 = __byte_perm(rw[0], rw[1], 0x5140), t1 = __byte_perm(rw[2], rw[3], 0x5140);
+        const uint32_t t2 = __byte_perm(rw[0], rw[1], 0x7362), t3 = __byte_perm(rw[2], rw[3], 0x7362);
+        uint8_t* vb = Vt + (4 * dq) * kPV + 4 * kq;
+        *reinterpret_cast<uint32_t*>(vb) = __byte_perm(t0, t1, 0x5410);
+        *reinterpret_cast<uint32_t*>(vb + kPV) = __byte_perm(t0, t1, 0x7632);
+        *reinterpret_cast<uint32_t*>(vb + 2 * kPV) = __byte_perm(t2, t3, 0x5410);
+        *reinterpret_cast<uint32_t*>(vb + 3 * kPV) = __byte_perm(t2, t3, 0x7632);
     }
     __syncthreads();
     const float s = p.s;
@@ -147,13 +163,19 @@ __global__ void __launch_bounds__(kThreads) attn_i8_kernel(const Params p) {
             }
         }
         __syncwarp();
-        // lane -> (row lane & 15, column half lane >> 4)
+        // lane -> (row lane & 15, column half lane >> 4); halves aligned to 4
+        // columns so S is read 16 bytes and P written 4 bytes at a time
         const int rr = lane & 15, hh = lane >> 4;
-        const int half = (L + 1) >> 1, c0 = hh * half, c1 = min(L, c0 + half);
+        const int half = ((((L + 1) >> 1) + 3) & ~3), c0 = hh * half, c1 = min(L, c0 + half);
         const int* Srow = Sw + rr * kPS;
         int mx = INT_MIN;
-#pragma unroll 4
-        for (int c = c0; c < c1; ++c) mx = max(mx, Srow[c]);
+        for (int c = c0; c < c1; c += 4) {
+            const int4 v4 = *reinterpret_cast<const int4*>(Srow + c);
+            mx = max(mx, v4.x);
+            if (c + 1 < c1) mx = max(mx, v4.y);
+            if (c + 2 < c1) mx = max(mx, v4.z);
+            if (c + 3 < c1) mx = max(mx, v4.w);
+        }
         mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
         int den = 0;
         uint8_t* Prow = P + rr * kPV;
@@ -162,11 +184,13 @@ __global__ void __launch_bounds__(kThreads) attn_i8_kernel(const Params p) {
         // 255 e^-x; any element within 5e-4 of a half-integer takes the fp64
         // definition, about 0.1% of them)
         for (int c = c0; c < c1; c += 4) {
+            const int4 v4 = *reinterpret_cast<const int4*>(Srow + c);
+            const int sv[4] = {v4.x, v4.y, v4.z, v4.w};
             uint32_t pc[4];
             bool near = false;
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                const int d = (c + i < c1) ? mx - Srow[c + i] : 1 << 21;
+                const int d = (c + i < c1) ? mx - sv[i] : 1 << 21;
                 const float x = __fmul_rn(c32, (float)d);
                 const float e = __fmul_rn(255.0f, __expf(-x));
                 const float r = rintf(e);
@@ -176,17 +200,12 @@ __global__ void __launch_bounds__(kThreads) attn_i8_kernel(const Params p) {
             if (near) {
 #pragma unroll 1
                 for (int i = 0; i < 4; ++i)
-                    if (c + i < c1) pc[i] = prob_code(c32, cc, mx - Srow[c + i]);
+                    if (c + i < c1) pc[i] = prob_code(c32, cc, mx - sv[i]);
             }
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                if (c + i < c1) {
-                    den += (int)pc[i];
-                    Prow[c + i] = (uint8_t)pc[i];
-                }
-            }
+            den += (int)(pc[0] + pc[1] + pc[2] + pc[3]);
+            *reinterpret_cast<uint32_t*>(Prow + c) = pc[0] | (pc[1] << 8) | (pc[2] << 16) | (pc[3] << 24);
         }
-        for (int c = L + hh; c < Lk; c += 2) Prow[c] = 0;   // padded keys
+        for (int c = ((L + 3) & ~3) + 4 * hh; c < Lk; c += 8) *reinterpret_cast<uint32_t*>(Prow + c) = 0u;   // padded keys
         den += __shfl_xor_sync(0xffffffffu, den, 16);
         const int den0 = __shfl_sync(0xffffffffu, den, g), den1 = __shfl_sync(0xffffffffu, den, g + 8);
         __syncwarp();
