@@ -57,36 +57,67 @@ def peaks():
     bf16_sus = float(p.get("bf16_tflops_sustained", 1400.0))
     # int8 dense = 2x bf16 dense (nominal 4.5 / 2.25 PFLOP/s; B200_PROFILING.md)
     return dict(src=src, hbm_gbs=hbm, int8_tops_burst=2 * bf16_burst, int8_tops_sustained=2 * bf16_sus,
-                bf16_tflops=bf16_burst)
+                bf16_tflops=bf16_burst, bf16_tflops_sustained=bf16_sus)
 
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock / power / throttle reasons sampled DURING the timed region:
+    NVML (pynvml) every 10 ms in a thread, nvidia-smi as the fallback."""
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
     def __init__(self, index=0):
         self.index = index
-        self.rows = []
+        self.rows = []          # (sm_mhz, max_mhz, power_w, set(reasons))
         self._stop = threading.Event()
         self._t = None
+        self.src = None
 
-    def _run(self):
+    def _nvml(self):
+        import pynvml as N
+        N.nvmlInit()
+        h = N.nvmlDeviceGetHandleByIndex(self.index)
+        bits = {"hw_slowdown": N.nvmlClocksEventReasonHwSlowdown,
+                "hw_thermal_slowdown": N.nvmlClocksEventReasonHwThermalSlowdown,
+                "sw_thermal_slowdown": N.nvmlClocksEventReasonSwThermalSlowdown,
+                "sw_power_cap": N.nvmlClocksEventReasonSwPowerCap}
+        mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+        self.src = "nvml"
+        while not self._stop.is_set():
+            sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+            pw = N.nvmlDeviceGetPowerUsage(h) / 1000.0
+            r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+            self.rows.append((float(sm), float(mx), pw, {k for k, b in bits.items() if r & b}))
+            self._stop.wait(0.01)
+
+    def _smi(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        self.src = "nvidia-smi"
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + q,
                                       "--format=csv,noheader,nounits"], capture_output=True, text=True,
                                      timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([c.strip() for c in out.split(",")])
+                c = [x.strip() for x in out.split(",")]
+                if len(c) >= 7:
+                    self.rows.append((float(c[0]), float(c[1]), float(c[2]),
+                                      {self.NAMES[i] for i in range(4) if c[3 + i] == "Active"}))
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.1)
+
+    def _run(self):
+        try:
+            self._nvml()
+        except Exception:
+            self._smi()
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
+        time.sleep(0.05)
         return self
 
     def __exit__(self, *a):
@@ -95,13 +126,22 @@ class ClockSampler:
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"], "samples": 0}
+        sm = [r[0] for r in self.rows]
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(r[1] for r in self.rows),
+                "sm_mhz_min": min(sm), "power_w_max": round(max(r[2] for r in self.rows), 1),
+                "reasons": sorted(set().union(*[r[3] for r in self.rows])), "samples": len(self.rows),
+                "source": self.src}
+
+
+def peak_regime(clk):
+    """'burst' if the timed region ran at (nearly) max SM clock with no power
+    cap, else 'sustained' (B200_PROFILING.md: the burst figure for a kernel
+    timed alone, the sustained one under the power cap)."""
+    sm, mx = clk.get("sm_mhz"), clk.get("sm_max_mhz")
+    if sm and mx and sm >= 0.95 * mx and "sw_power_cap" not in clk.get("reasons", []):
+        return "burst"
+    return "sustained"
 
 
 # ------------------------------------------------------------------ our arm
@@ -117,7 +157,7 @@ def setup_layer(torch, dev, rank):
     return L, p
 
 
-def stage_calls(M, L, h_in, ws, T, stream):
+def stage_calls(M, L, h_in, B, T, stream):
     """The eight launches of mkq_bert_layer as separate C-ABI calls (same
     kernels, same arguments) so each can be bracketed by CUDA events."""
     import torch
@@ -136,7 +176,7 @@ def stage_calls(M, L, h_in, ws, T, stream):
     buf["f"] = torch.empty((T, hd), dtype=torch.float32, device=dev)
     buf["out"] = torch.empty((T, hd), dtype=torch.float32, device=dev)
     sq = torch.tensor([s["s_qkv_in"]], device=dev)
-    B, S = CFG["batch"], CFG["seq"]
+    S = CFG["seq"]
     calls = [
         ("quantize_in", lambda: M.mkq_quantize_pack(h_in, sq, 4, -8, 7, out=buf["c_in"], stream=stream), 0),
         ("gemm_qkv", lambda: M.mkq_gemm_w4a4(buf["c_in"], t["w_qkv"], s["s_qkv_in"], t["sw_qkv"], t["b_qkv"],
@@ -149,7 +189,7 @@ def stage_calls(M, L, h_in, ws, T, stream):
                                                        s_q=s["s_ffn1_in"], y=buf["h1"], q=buf["c_h1"], stream=stream), 0),
         ("gemm_ffn1", lambda: M.mkq_gemm_w4a4(buf["c_h1"], t["w_1"], s["s_ffn1_in"], t["sw_1"], t["b_1"],
                                               mode=M.OUT_I4, gelu=True, s_out=s["s_ffn2_in"], out=buf["a2"], K=hd,
-                                              stream=stream), 2.0 * T * hd * F),
+                                              stream=stream, requant_table=L.table), 2.0 * T * hd * F),
         ("gemm_ffn2", lambda: M.mkq_gemm_w4a4(buf["a2"], t["w_2"], s["s_ffn2_in"], t["sw_2"], t["b_2"],
                                               mode=M.OUT_F32, out=buf["f"], K=F, stream=stream), 2.0 * T * hd * F),
         ("ln2", lambda: M.mkq_residual_layernorm(buf["f"], buf["h1"], t["ln2_g"], t["ln2_b"], L.ln_eps,
@@ -159,20 +199,20 @@ def stage_calls(M, L, h_in, ws, T, stream):
 
 
 def load_traffic():
-    """Per-launch DRAM bytes of each stage from the committed ncu --set full
-    summary (tools/summarize_ncu.py -> profiles/r*_layer_traffic.json)."""
+    """Per-launch DRAM bytes of each stage from the newest committed ncu
+    --set full summary (tools/summarize_ncu.py -> profiles/r*_layer_traffic.json)."""
     import glob
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_layer_traffic.json")))
     if not files:
-        return {}
+        return {}, None
     try:
-        return json.load(open(files[-1]))
+        return json.load(open(files[-1])), os.path.relpath(files[-1], ROOT)
     except Exception:
-        return {}
+        return {}, None
 
 
 def stage_bytes(T, hd, F):
-    """Algorithmic HBM bytes per launch (DESIGN.md §6)."""
+    """Algorithmic HBM bytes per launch (DESIGN.md §5)."""
     return {
         "quantize_in": T * hd * 4.5,
         "gemm_qkv": T * hd / 2 + 3 * hd * hd / 2 + T * 3 * hd * 2,
@@ -185,9 +225,49 @@ def stage_bytes(T, hd, F):
     }
 
 
+def event_time(torch, fn, stream, reps, warm=2):
+    """Mean device time (ms) of fn() over reps back-to-back calls on stream."""
+    with torch.cuda.stream(stream):
+        for _ in range(warm):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            fn()
+        e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def graph_time(torch, fn, dev, reps=100, inner=1):
+    """Device time (ms) per fn() call: `inner` calls captured in one CUDA graph,
+    replayed reps // inner times (the paper's mean of 100 rounds, P:252)."""
+    st = torch.cuda.Stream(device=dev)
+    with torch.cuda.stream(st):
+        for _ in range(3):
+            fn(st)
+        torch.cuda.synchronize(dev)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            for _ in range(inner):
+                fn(st)
+        g.replay()
+        torch.cuda.synchronize(dev)
+        n = max(1, reps // inner)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(n):
+            g.replay()
+        e1.record(st)
+    torch.cuda.synchronize(dev)
+    return e0.elapsed_time(e1) / (n * inner)
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
+    from paper_2203_13483_b200 import dist as D
     from paper_2203_13483_b200 import mkq as M
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -195,15 +275,21 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     import synth
 
     L, p = setup_layer(torch, dev, rank)
-    B, S, hd, F = CFG["batch"], CFG["seq"], CFG["hidden"], CFG["ffn"]
+    S, hd, F = CFG["seq"], CFG["hidden"], CFG["ffn"]
+    B_total = CFG["batch"]
+    if args.scaling == "strong":   # the BASELINE configs[3] batch, whole sequences sharded over the ranks
+        b0, b1 = D.row_shard(B_total, world, rank)
+        B = b1 - b0
+    else:                          # every rank runs a full configs[3] batch
+        b0, B = rank * B_total, B_total
     T = B * S
-    h_host = synth.hidden_states(B, S, hd, seed=rank)
+    h_host = synth.hidden_states(B, S, hd, seed=1 + b0)
     h_in = torch.from_numpy(h_host).to(dev)
     h_out = torch.empty_like(h_in)
     ws = torch.empty(L.workspace_size(T), dtype=torch.uint8, device=dev)
@@ -217,13 +303,19 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize(dev)
 
+    def max_ranks(x):
+        if world == 1:
+            return x
+        tt = torch.tensor([x], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        return float(tt.item())
+
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
             step()
     barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
-        time.sleep(0.3)
         barrier()
         ev0.record(stream)
         for _ in range(args.steps):
@@ -231,16 +323,15 @@ def run_ours(args):
         ev1.record(stream)
         barrier()
     ms = ev0.elapsed_time(ev1) / args.steps
-    t_max = ms
-    if world > 1:
-        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_max = float(tt.item())
-    ops = linear_ops(T, hd, F)
-    value = world * ops / (t_max * 1e-3) / 1e12
+    t_max = max_ranks(ms)
+    tokens_all = (B_total if args.scaling == "strong" else B_total * world) * S
+    ops_all = linear_ops(tokens_all, hd, F)
+    value = ops_all / (t_max * 1e-3) / 1e12
+    clocks = clk.summary()
+    regime = peak_regime(clocks)
 
-    # ---- per-stage device times (same kernels, one event pair per launch)
-    calls, buf = stage_calls(M, L, h_in, ws, T, stream)
+    # ---- per-stage device times (same kernels, one event pair per launch; rank 0's shard)
+    calls, buf = stage_calls(M, L, h_in, B, T, stream)
     nrep = max(3, min(args.steps, 10))
     evs = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in calls]
            for _ in range(nrep)]
@@ -262,29 +353,38 @@ def run_ours(args):
     gemms = {k: v for k, v in stage_ms.items() if k.startswith("gemm")}
     dom = max(stage_ms, key=stage_ms.get)
     ops_of = {c[0]: c[2] for c in calls}
-    traffic = load_traffic()
+    traffic, traffic_src = load_traffic()
+    i8 = {"burst": pk["int8_tops_burst"], "sustained": pk["int8_tops_sustained"]}
+    f16 = {"burst": pk["bf16_tflops"], "sustained": pk["bf16_tflops_sustained"]}
 
     def roofline(k):
         tr = traffic.get(k, {}).get("dram_bytes")
-        if k == "attention":   # fp16 tensor-core contraction (mma.sync), flops = 4*T*S*d
+        base = {"kernel": k, "traffic": tr, "traffic_src": traffic_src, "algorithmic_bytes": sb[k],
+                "peak_regime": regime}
+        if ops_of[k] > 0:
             ach = ops_of[k] / (stage_ms[k] * 1e-3) / 1e12
-            return {"kernel": k, "bound": "tensor", "achieved": round(ach, 1), "peak": round(pk["bf16_tflops"], 1),
-                    "unit": "TFLOP/s (fp16 dense)", "frac": round(ach / pk["bf16_tflops"], 4),
-                    "traffic": tr, "algorithmic_bytes": sb[k],
-                    "peak_src": f"{pk['src']} bf16_tflops (burst; fp16 = bf16 nominal rate)"}
-        if ops_of[k] > 0:      # int8 tensor-core contraction (tcgen05 kind::i8)
-            ach = ops_of[k] / (stage_ms[k] * 1e-3) / 1e12
-            return {"kernel": k, "bound": "tensor", "achieved": round(ach, 1),
-                    "peak": round(pk["int8_tops_sustained"], 1), "unit": "TOPS (int8 dense)",
-                    "frac": round(ach / pk["int8_tops_sustained"], 4), "traffic": tr, "algorithmic_bytes": sb[k],
-                    "peak_src": f"{pk['src']} bf16_tflops_sustained x2 (int8:bf16 nominal 4.5:2.25)"}
+            if k == "attention":   # fp16 tensor-core contraction, flops = 4*T*S*d
+                pk_ = f16
+                base.update(unit="TFLOP/s (fp16 dense)",
+                            peak_src=f"{pk['src']} bf16_tflops{'' if regime == 'burst' else '_sustained'} "
+                                     f"(fp16 = bf16 nominal rate)")
+            else:                  # int8 tensor-core contraction (tcgen05 kind::i8)
+                pk_ = i8
+                base.update(unit="TOPS (int8 dense)",
+                            peak_src=f"{pk['src']} 2 x bf16_tflops{'' if regime == 'burst' else '_sustained'} "
+                                     f"(int8:bf16 nominal 4.5:2.25)")
+            base.update(bound="tensor", achieved=round(ach, 1), peak=round(pk_[regime], 1),
+                        frac=round(ach / pk_[regime], 4), frac_of_burst=round(ach / pk_["burst"], 4),
+                        frac_of_sustained=round(ach / pk_["sustained"], 4))
+            return base
         ach = sb[k] / (stage_ms[k] * 1e-3) / 1e9
-        return {"kernel": k, "bound": "hbm", "achieved": round(ach, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
-                "frac": round(ach / pk["hbm_gbs"], 4), "traffic": tr, "algorithmic_bytes": sb[k],
-                "peak_src": pk["src"] + " hbm_gbs"}
+        base.update(bound="hbm", achieved=round(ach, 1), peak=pk["hbm_gbs"], unit="GB/s",
+                    frac=round(ach / pk["hbm_gbs"], 4), peak_src=pk["src"] + " hbm_gbs")
+        return base
 
     roof = roofline(dom)
-    roof_all = {k: {kk: v for kk, v in roofline(k).items() if kk in ("bound", "achieved", "unit", "frac")}
+    roof_all = {k: {kk: v for kk, v in roofline(k).items()
+                    if kk in ("bound", "achieved", "unit", "frac", "frac_of_burst", "frac_of_sustained")}
                 for k in stage_ms}
     stages = {}
     for k, v in stage_ms.items():
@@ -292,20 +392,19 @@ def run_ours(args):
              "gbs": round(sb[k] / (v * 1e-3) / 1e9, 1)}
         if ops_of[k]:
             d["tops"] = round(ops_of[k] / (v * 1e-3) / 1e12, 1)
-            d["frac_int8_peak"] = round(ops_of[k] / (v * 1e-3) / 1e12 / pk["int8_tops_sustained"], 3)
         stages[k] = d
     gemm_ms = sum(gemms.values())
-    gemm_tops = ops / (gemm_ms * 1e-3) / 1e12
+    gemm_tops = linear_ops(T, hd, F) / (gemm_ms * 1e-3) / 1e12
 
     # ---- e2e: host buffers through the C-ABI, H2D + layer + D2H in the timed region.
-    # Whole sequences are independent, so the batch is processed in chunks of
-    # sequences pipelined over three streams (H2D of chunk i+1 and D2H of
+    # Whole sequences are independent, so the rank's batch is processed in chunks
+    # of sequences pipelined over three streams (H2D of chunk i+1 and D2H of
     # chunk i-1 overlap the layer on chunk i); the result is bit-identical to
     # one call on the whole batch (checked below).
     h_pin = torch.from_numpy(h_host).pin_memory()
     o_pin = torch.empty(h_host.shape, dtype=torch.float32).pin_memory()
     e2e_steps = max(2, min(args.steps, 5))
-    nch = 8 if B % 8 == 0 else 1
+    nch = 8 if B % 8 == 0 and B >= 16 else 1
     Bc, Tc = B // nch, (B // nch) * S
     ws_c = torch.empty(L.workspace_size(Tc), dtype=torch.uint8, device=dev)
     s_in, s_out = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
@@ -330,7 +429,9 @@ def run_ours(args):
     e2e_step()
     barrier()
     e2e_same = bool(np.array_equal(o_pin.numpy(), buf["out"].cpu().numpy()))
+    del buf
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
     e0.record(stream)
     s_in.wait_stream(stream)
     for _ in range(e2e_steps):
@@ -338,27 +439,25 @@ def run_ours(args):
     stream.wait_stream(s_out)
     e1.record(stream)
     barrier()
-    e2e_ms = e0.elapsed_time(e1) / e2e_steps
+    e2e_ms = max_ranks(e0.elapsed_time(e1) / e2e_steps)
+    del ws_c, h_pin, o_pin
+
+    # ---- multi-GPU arms (every rank): C3 row-sharded encoder, column-parallel FFN (N > 1)
+    c3_rs = c3_row_sharded(torch, dev, world, rank, barrier, max_ranks)
+    colpar = None
     if world > 1:
-        tt = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_ms = float(tt.item())
+        colpar = column_parallel_ffn(torch, L, dev, world, rank, barrier, max_ranks, stream)
+    del h_out, ws
 
-    # ---- paper-style comparison arm: fp32 / bf16 torch layer
-    cmp = None
-    if rank == 0 and not args.no_compare:
-        cmp = compare_float_layers(torch, p, dev, ms, args)
-
-    t2 = None
-    if rank == 0 and not args.no_table2:
-        t2 = table2(torch, dev)
-
-    qat = None
-    if rank == 0:
-        qat = qat_calibration(torch, M, h_in, stream, pk)
-    c3 = None
-    if rank == 0 and not args.no_table2:
-        c3 = c3_encoder(torch, dev)
+    extras = {}
+    if rank == 0 and world == 1 and not args.no_extras:
+        extras["small_configs_c1_c2"] = small_configs(torch, dev, pk, regime)
+        if not args.no_compare:
+            extras["paper_comparison"] = compare_float_layers(torch, p, dev, ms, args)
+        if not args.no_table2:
+            extras["table2_bert_base_varlen"] = table2(torch, dev)
+            extras["bert_base_12l_b32s128"] = c3_encoder(torch, dev)
+        extras["qat_and_calibration"] = qat_calibration(torch, M, h_in, stream, pk)
 
     result = None
     if rank == 0:
@@ -372,37 +471,183 @@ def run_ours(args):
             "warmup": args.warmup,
             "ms_per_step": round(t_max, 4),
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": args.scaling,
             "vs_baseline": None,
             "dtype": "s4 x s4 -> s32 (int8 tcgen05), fp32 epilogue/LN, fp16 attention",
             "data": "synthetic (seeded N(0,1) activations, N(0,0.02^2) random-init BERT weights)",
-            "config": {"workload": WORKLOAD, "batch_per_rank": B, "seq_len": S, "hidden": hd, "heads": CFG["heads"],
-                       "ffn": F, "bits": 4, "tokens_per_rank": T, "parallelism": f"row-shard x{world} (no collective)",
-                       "l2": "inputs > L2: 537 MB fp32 activations + ~3 GB intermediates per step; weights (6.3 MB) L2-resident"},
+            "config": {"workload": WORKLOAD, "batch_total": B_total if args.scaling == "strong" else B_total * world,
+                       "batch_per_rank": B, "seq_len": S, "hidden": hd, "heads": CFG["heads"], "ffn": F, "bits": 4,
+                       "tokens_per_rank": T,
+                       "parallelism": f"row-shard x{world} by whole sequences ({args.scaling} scaling, no collective)",
+                       "l2": "inputs > L2: 537 MB fp32 activations per full batch + ~3 GB intermediates; "
+                             "weights (6.3 MB) L2-resident"},
             "layer_latency_us": round(t_max * 1e3, 1),
             "gemm_only_tops": round(gemm_tops, 1),
             "stages": stages,
             "layer_equals_staged": same,
             "roofline": roof,
             "roofline_by_stage": roof_all,
-            "e2e": {"value": round(world * ops / (e2e_ms * 1e-3) / 1e12, 2), "unit": "TOPS",
+            "e2e": {"value": round(ops_all / (e2e_ms * 1e-3) / 1e12, 2), "unit": "TOPS",
                     "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": int(h_host.nbytes),
                     "d2h_bytes_per_step": int(h_host.nbytes),
-                    "pipeline": f"{nch} chunks of {Bc} sequences over H2D / compute / D2H streams",
+                    "pipeline": f"{nch} chunks of {Bc} sequences per rank over H2D / compute / D2H streams",
                     "result_equals_device_step": e2e_same},
             "gpu_launches": 8 * args.steps,
-            "clocks": clk.summary(),
+            "clocks": clocks,
             "cpu_baseline": cpu,
-            "paper_comparison": cmp,
-            "table2_bert_base_varlen": t2,
-            "qat_and_calibration": qat,
-            "bert_base_12l_b32s128": c3,
+            "c3_row_sharded": c3_rs,
+            "column_parallel_ffn": colpar,
         }
-        print(json.dumps(result))
+        result.update(extras)
+        print(json.dumps(result), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
     return result
+
+
+def c3_row_sharded(torch, dev, world, rank, barrier, max_ranks, reps=20):
+    """BASELINE.json configs[2] row-sharded: the BERT-base
+    12-layer mixed-precision encoder (layers 1-6 W8A8, 7-12 W4A4)
+    over the batch of 32 x 128-token sequences, 32/g whole sequences per
+    rank, no collective; one CUDA graph per rank, max over ranks."""
+    import synth
+    from paper_2203_13483_b200 import dist as D
+    from paper_2203_13483_b200 import model
+    h, H, F, Btot, S = 768, 12, 3072, 32, 128
+    b0, b1 = D.row_shard(Btot, world, rank)
+    B = b1 - b0
+    layers = []
+    for i, bits in enumerate(model.bit_plan(12, 6)):
+        p = synth.layer_params(h, H, F, i)
+        L = model.build_layer(p, bits, dev)
+        model.calibrate(L, torch.from_numpy(synth.hidden_states(4, S, h, seed=1000000 + i)).to(dev), 4, S)
+        layers.append(L)
+    enc = model.Encoder(layers)
+    hin = torch.from_numpy(synth.hidden_states(B, S, h, seed=1 + b0)).to(dev)
+    out = torch.empty_like(hin)
+    barrier()
+    ms = graph_time(torch, lambda st: enc(hin, B, S, out=out, stream=st), dev, reps=reps)
+    t = max_ranks(ms)
+    T = Btot * S
+    return {"workload": "BERT-base 12 layers, 6 x W8A8 + 6 x W4A4, batch 32 x seq 128 (configs[2])",
+            "n_gpus": world, "sequences_per_rank": B, "ms": round(t, 4),
+            "tokens_per_s": round(T / (t * 1e-3), 1),
+            "tops": round(12 * linear_ops(T, h, F) / (t * 1e-3) / 1e12, 1), "scaling": "strong",
+            "timing": "CUDA graph of the 12-layer stack per rank, mean of replays, max over ranks"}
+
+
+def column_parallel_ffn(torch, L, dev, world, rank, barrier, max_ranks, stream, reps=5):
+    """BASELINE.json configs[3] column-parallel FFN: every rank
+    holds W^1 rows [rF/g, (r+1)F/g) and W^2 rows [rh/g, (r+1)h/g) and
+    processes ALL 131072 tokens; FFN1 (GELU + int4 requant fused) -> NCCL
+    all_gather of the packed int4 codes -> interleave -> FFN2 -> NCCL
+    all_gather of the fp32 output columns -> interleave -> residual + LN2.
+    Each sub-step is timed with CUDA events on its stream; all-gather
+    bandwidth is reported as NCCL's busbw against the measured 770 GB/s
+    per-direction NVLink peer figure (B200_PROFILING.md)."""
+    import synth
+    import torch.distributed as dist
+    from paper_2203_13483_b200 import dist as D
+    from paper_2203_13483_b200 import mkq as M
+    hd, F, S = L.hidden, L.ffn, CFG["seq"]
+    T = CFG["batch"] * S
+    cp = D.ColumnParallelFFN(L, rank, world)
+    h1 = torch.from_numpy(synth.hidden_states(CFG["batch"], S, hd, seed=7)).to(dev)
+    codes = M.mkq_quantize_pack(h1, torch.tensor([L.scales["s_ffn1_in"]], device=dev), 4, -8, 7)
+    names = ("ffn1_local", "allgather_int4", "interleave_int4", "ffn2_local", "allgather_f32", "interleave_f32",
+             "ln2")
+    times = {n: [] for n in names}
+
+    def once(record):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(names) + 1)]
+        with torch.cuda.stream(stream):
+            ev[0].record(stream)
+            a_loc = cp.ffn1_local(codes, stream)
+            ev[1].record(stream)
+            a_blk = D.gather_blocks(a_loc, world)
+            ev[2].record(stream)
+            a2 = M.mkq_interleave_blocks(a_blk, world, T, a_loc.shape[1], stream=stream)
+            ev[3].record(stream)
+            f_loc = cp.ffn2_local(a2, stream)
+            ev[4].record(stream)
+            f_blk = D.gather_blocks(f_loc, world)
+            ev[5].record(stream)
+            f = M.mkq_interleave_blocks(f_blk.view(torch.uint8), world, T, cp.hl * 4, stream=stream).view(torch.float32)
+            ev[6].record(stream)
+            out = M.mkq_residual_layernorm(f, h1, L.t["ln2_g"], L.t["ln2_b"], L.ln_eps, stream=stream)
+            ev[7].record(stream)
+        torch.cuda.synchronize(dev)
+        if record:
+            for i, n in enumerate(names):
+                times[n].append(ev[i].elapsed_time(ev[i + 1]))
+        return out
+
+    once(False)
+    barrier()
+    for _ in range(reps):
+        barrier()
+        once(True)
+    ms = {n: max_ranks(float(np.mean(v))) for n, v in times.items()}
+    tot = max_ranks(float(np.sum([np.mean(v) for v in times.values()])))
+    g1 = T * F / 2          # bytes of the gathered int4 FFN2 input
+    g2 = T * hd * 4         # bytes of the gathered fp32 FFN2 output
+    busbw = lambda nbytes, t: nbytes / (t * 1e-3) / 1e9 * (world - 1) / world  # noqa: E731
+    ops = 2 * 2.0 * T * hd * F
+    # bit-exactness of the sharded FFN against the single-GPU FFN on rank 0's rows is covered by
+    # tests/test_gpu_dist.py and tests/test_dist_cpu.py (gloo); here: timing only
+    return {"workload": "BERT-large FFN block (h 1024, F 4096) over 256 x 512 tokens, column-parallel x"
+                        f"{world} (configs[3])",
+            "ms_total": round(tot, 4), "ffn_tops": round(ops / (tot * 1e-3) / 1e12, 1),
+            "stages_ms": {k: round(v, 4) for k, v in ms.items()},
+            "allgather_int4": {"bytes": int(g1), "busbw_gbs": round(busbw(g1, ms["allgather_int4"]), 1)},
+            "allgather_f32": {"bytes": int(g2), "busbw_gbs": round(busbw(g2, ms["allgather_f32"]), 1)},
+            "nvlink_ref_gbs": 770.0, "collective": "NCCL all_gather_into_tensor (torch.distributed)"}
+
+
+def small_configs(torch, dev, pk, regime):
+    """BASELINE.json configs[0] (one W4A4 linear M=128, K=N=768, per-tensor
+    act scale + per-channel weight scale, bias, fp32 out) and configs[1]
+    (BERT-base W4A4 layer, batch 1 x seq 128), each the mean of 100 rounds
+    (P:252), graph-timed; everything is L2-resident at these sizes."""
+    import synth
+    from paper_2203_13483_b200 import mkq as M
+    from paper_2203_13483_b200 import model
+    out = {}
+    Mr, K, N = 128, 768, 768
+    x = torch.from_numpy(synth.activations(Mr, K, seed=0)).to(dev)
+    w = torch.from_numpy(synth.weight(N, K, seed=1)).to(dev)
+    b = torch.from_numpy(synth.bias(N, 1)).to(dev)
+    wq, sw = model.prepare_weight(w, 4)
+    s_a = 0.5558
+    a = M.mkq_quantize_pack(x, torch.tensor([s_a], device=dev), 4, -8, 7)
+    y = torch.empty((Mr, N), dtype=torch.float32, device=dev)
+    f = lambda st: M.mkq_gemm_w4a4(a, wq, s_a, sw, b, mode=M.OUT_F32, out=y, stream=st)  # noqa: E731
+    t1 = graph_time(torch, f, dev, reps=100, inner=1)
+    t100 = graph_time(torch, f, dev, reps=100, inner=100)
+    ops = 2.0 * Mr * N * K
+    nbytes = Mr * K / 2 + N * K / 2 + Mr * N * 4 + 8 * N
+    i8 = pk["int8_tops_burst"] if regime == "burst" else pk["int8_tops_sustained"]
+    out["c1_linear_m128_k768_n768"] = {
+        "us_per_call_single_graph_replay": round(t1 * 1e3, 2), "us_per_call_back_to_back": round(t100 * 1e3, 2),
+        "tops": round(ops / (t100 * 1e-3) / 1e12, 2), "frac_int8_peak": round(ops / (t100 * 1e-3) / 1e12 / i8, 4),
+        "gbs": round(nbytes / (t100 * 1e-3) / 1e9, 1), "frac_hbm": round(nbytes / (t100 * 1e-3) / 1e9 / pk["hbm_gbs"], 4),
+        "bound": "latency (0.74 MB, 0.15 G ops: t_TC 0.03 us, t_HBM 0.1 us vs ~2 us launch+pipeline fill)"}
+    h, H, Fh, S = 768, 12, 3072, 128
+    p = synth.layer_params(h, H, Fh, 0)
+    L = model.build_layer(p, 4, dev)
+    model.calibrate(L, torch.from_numpy(synth.hidden_states(8, S, h, seed=1000000)).to(dev), 8, S)
+    hin = torch.from_numpy(synth.hidden_states(1, S, h, seed=1)).to(dev)
+    ho = torch.empty_like(hin)
+    ws = torch.empty(L.workspace_size(S), dtype=torch.uint8, device=dev)
+    g = lambda st: M.mkq_bert_layer(L, hin, 1, S, None, h_out=ho, ws=ws, stream=st)  # noqa: E731
+    tl1 = graph_time(torch, g, dev, reps=100, inner=1)
+    tl = graph_time(torch, g, dev, reps=100, inner=20)
+    out["c2_bert_base_layer_b1_s128"] = {
+        "us_per_layer_single_graph_replay": round(tl1 * 1e3, 2), "us_per_layer_back_to_back": round(tl * 1e3, 2),
+        "effective_tops": round(linear_ops(S, h, Fh) / (tl * 1e-3) / 1e12, 2), "kernels_per_layer": 8,
+        "bound": "latency: 8 dependent kernels at M = 128 (PDL overlaps prologues)"}
+    return out
 
 
 def c3_encoder(torch, dev, reps=20):
@@ -534,7 +779,7 @@ def table2(torch, dev, reps=50):
     (h 768, 12 heads, FFN 3072) over BS sequences of max length 128 with the
     given number of valid (non-padding) tokens, packed (cu_seqlens, R13);
     int4 (W4A4) and int8 (W8A8) layers through mkq_bert_layer captured in a
-    CUDA graph, fp32 (TF32 off) torch/cuBLAS layer on the padded batch;
+    CUDA graph, fp32 (TF32 off) torch/cuBLAS layer on the valid tokens;
     mean of `reps` CUDA-graph replays / eager runs."""
     import synth
     import torch.nn.functional as Fn
@@ -578,18 +823,22 @@ def table2(torch, dev, reps=50):
             e1.record()
             torch.cuda.synchronize(dev)
             res[f"{key}_us"] = round(e0.elapsed_time(e1) / reps * 1e3, 1)
-        # fp32 torch layer on the padded batch (key padding mask)
-        x = torch.zeros(bs, S, h, device=dev)
+        # fp32 torch/cuBLAS layer on the VALID tokens (like for like with the packed int4 layer):
+        # linears, GELU and LayerNorms on the packed [valid, h] rows; attention (a small share at
+        # s <= 128) on the padded [bs, 128] batch with a key mask, pad / unpad gathers included
         mask = torch.zeros(bs, S, dtype=torch.bool, device=dev)
         for i, Lq in enumerate(lens):
             mask[i, :Lq] = True
+        idx = mask.view(-1).nonzero().squeeze(1)
         am = torch.where(mask[:, None, None, :], 0.0, float("-inf"))
+        x = torch.from_numpy(synth.hidden_states(1, valid, h, seed=1)).to(dev)
 
         def layer32(xx):
-            qkv = Fn.linear(xx, W["w_qkv"], W["b_qkv"]).view(bs, S, 3, H, 64)
-            q, k, v = qkv.unbind(2)
+            qkv = Fn.linear(xx, W["w_qkv"], W["b_qkv"])
+            pad = torch.zeros(bs * S, 3 * h, device=dev).index_copy_(0, idx, qkv).view(bs, S, 3, H, 64)
+            q, k, v = pad.unbind(2)
             a = Fn.scaled_dot_product_attention(q.transpose(1, 2), k.transpose(1, 2), v.transpose(1, 2), attn_mask=am)
-            a = a.transpose(1, 2).reshape(bs, S, h)
+            a = a.transpose(1, 2).reshape(bs * S, h).index_select(0, idx)
             h1 = Fn.layer_norm(Fn.linear(a, W["w_o"], W["b_o"]) + xx, (h,), W["ln1_g"], W["ln1_b"], 1e-12)
             f = Fn.linear(Fn.gelu(Fn.linear(h1, W["w_1"], W["b_1"])), W["w_2"], W["b_2"])
             return Fn.layer_norm(f + h1, (h,), W["ln2_g"], W["ln2_b"], 1e-12)
@@ -614,6 +863,23 @@ def table2(torch, dev, reps=50):
 
 
 # ------------------------------------------------------------------ oracle (CPU) arm
+def host_info():
+    """nproc, the affinity mask size and the CPU model of the host the oracle ran on."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    try:
+        aff = len(os.sched_getaffinity(0))
+    except Exception:
+        aff = None
+    return {"nproc": os.cpu_count(), "affinity_cpus": aff, "cpu_model": model, "threads_used": 1}
+
+
 def cpu_baseline(sample_seqs=1):
     """The oracle as it stands, on the host cores, over a bounded sample of
     the same workload (whole sequences of the BERT-large layer)."""
@@ -634,6 +900,7 @@ def cpu_baseline(sample_seqs=1):
     dt = time.perf_counter() - t0
     T = sample_seqs * S
     return {"value": round(linear_ops(T, hd, F) / dt / 1e12, 6), "unit": "TOPS", "cores": 1, "kind": "oracle",
+            "host": host_info(),
             "sample": f"{sample_seqs} x {S}-token sequence(s) of the BERT-large W4A4 layer (oracle/: scalar C int "
                       f"GEMM + fp64 NumPy glue, single thread), {dt:.2f} s",
             "seconds": round(dt, 3)}
@@ -655,11 +922,11 @@ def run_reference(args):
         "impl": "reference",
         "metric": "W4A4 GEMM TOPS (effective: layer linear-GEMM int ops / BERT int4 layer time)",
         "value": round(v, 6), "unit": "TOPS", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(sec * 1e3, 1), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": round(sec * 1e3, 1), "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
         "dtype": "s4 x s4 -> s32 (scalar C), fp64 glue", "data": "synthetic",
         "config": {"workload": WORKLOAD, "sample": "1 sequence of 512 tokens per step"},
         "cpu_baseline": {"value": round(v, 6), "unit": "TOPS", "cores": 1, "kind": "oracle",
-                         "sample": "1 x 512-token sequence per step"},
+                         "sample": "1 x 512-token sequence per step", "host": host_info()},
         "e2e": {"value": round(v, 6), "unit": "TOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(res))
@@ -675,13 +942,31 @@ def main():
     ap.add_argument("--no-compare", action="store_true", help="skip the fp32/bf16 torch comparison layer")
     ap.add_argument("--no-cpu", action="store_true", help="skip the oracle cpu_baseline")
     ap.add_argument("--no-table2", action="store_true", help="skip the paper Table 2 (BERT-base varlen) rows")
+    ap.add_argument("--no-extras", action="store_true", help="only the headline line (no single-GPU extra sections)")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong: the configs[3] batch (256 x 512) sharded over the ranks (default); "
+                         "weak: a full batch per rank")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(relaunch(args.gpus))
     if args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)
+
+
+def relaunch(n: int) -> int:
+    """`bench.py --gpus N` outside torchrun: start N ranks (one per GPU)
+    through torch.distributed.run on 127.0.0.1 and return its exit code."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 if __name__ == "__main__":

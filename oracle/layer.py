@@ -14,8 +14,10 @@ where Q is Eq.1 with the static per-tensor activation scale, every
 Linear is the integer GEMM + dequant of oracle.linear, GELU is gelu_pinned
 (R7) fused with the requantize of the FFN2 input (a5, a6), LayerNorm and
 softmax are computed in float64 (P:234 asks for >= float32) and attention
-takes q, k, v rounded to fp16 (R10: the precision the product declares for
-its attention operands).
+takes q, k, v as the fp32 dequant outputs of the QKV linear (SURVEY §8(c)
+O-L; P:234 keeps the glue in float32).  The product's fp16 attention
+operands (R10) are a product property with their own stated
+tolerance in the GPU tests; they are not mirrored here.
 
 Parity status: the bit-exact linear steps are pinned in tests/test_oracle.py;
 the fp64 glue (attention, LN) is pinned by closed forms (softmax rows sum to
@@ -28,7 +30,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from . import (A4, A8, W4, W8, OUT_F16, OUT_F32, OUT_I4, OUT_I8, absmax_scale,
+from . import (A4, A8, W4, W8, OUT_F32, OUT_I4, OUT_I8, absmax_scale,
                act_scale, linear, quantize)
 
 LN_EPS = 1e-12
@@ -77,7 +79,7 @@ class LayerWeights:
     s_ffn1_in: np.float32 = np.float32(1)
     s_ffn2_in: np.float32 = np.float32(1)
     # NEXT(2) integer attention core (R19): scale of the int8 q|k|v codes;
-    # None = fp16 attention operands (R10)
+    # None = float attention on the fp32 q|k|v (SURVEY O-L)
     s_attn: object = None
 
 
@@ -94,11 +96,6 @@ def softmax(s: np.ndarray) -> np.ndarray:
     s = np.asarray(s, dtype=np.float64)
     e = np.exp(s - s.max(axis=-1, keepdims=True))
     return e / e.sum(axis=-1, keepdims=True)
-
-
-def f16_round(x: np.ndarray) -> np.ndarray:
-    """RN-even to binary16 and back (R10); numpy's cast is correctly rounded."""
-    return np.asarray(x, dtype=np.float32).astype(np.float16).astype(np.float64)
 
 
 def attention_int8(codes: np.ndarray, seqlens, heads: int, s_qkv) -> np.ndarray:
@@ -171,7 +168,7 @@ def attention(qkv: np.ndarray, seqlens, heads: int) -> np.ndarray:
 @dataclass
 class LayerTrace:
     codes_in: np.ndarray = None
-    qkv: np.ndarray = None        # fp16-rounded q,k,v as float64
+    qkv: np.ndarray = None        # fp32 q|k|v (int8 codes with s_attn)
     oa: np.ndarray = None         # fp32
     codes_oa: np.ndarray = None
     o: np.ndarray = None          # fp32 (W^A output incl. bias)
@@ -194,9 +191,8 @@ def bert_layer(h: np.ndarray, W: LayerWeights, seqlens) -> LayerTrace:
                        s_out=W.s_attn, qmin_out=-127, qmax_out=127)
         T.oa = attention_int8(T.qkv, seqlens, W.heads, W.s_attn)
     else:
-        qkv16 = linear(T.codes_in, W.qkv.codes, W.s_qkv_in, W.qkv.s_w, W.qkv.bias, mode=OUT_F16)
-        T.qkv = qkv16.view(np.float16).astype(np.float64)
-        T.oa = attention(T.qkv, seqlens, W.heads).astype(np.float32)
+        T.qkv = linear(T.codes_in, W.qkv.codes, W.s_qkv_in, W.qkv.s_w, W.qkv.bias, mode=OUT_F32)
+        T.oa = attention(T.qkv.astype(np.float64), seqlens, W.heads).astype(np.float32)
     T.codes_oa = quantize(T.oa, W.s_o_in, lo, hi)
     T.o = linear(T.codes_oa, W.o.codes, W.s_o_in, W.o.s_w, W.o.bias, mode=OUT_F32)
     T.h1 = layernorm(T.o.astype(np.float64) + h, W.ln1_g, W.ln1_b).astype(np.float32)
@@ -226,9 +222,8 @@ def calibrate(h_calib: np.ndarray, W: LayerWeights, seqlens, int_attention: bool
                       qmin_out=-127, qmax_out=127)
         oa = attention_int8(qkv8, seqlens, W.heads, W.s_attn)
     else:
-        qkv = linear(codes, W.qkv.codes, W.s_qkv_in, W.qkv.s_w, W.qkv.bias,
-                     mode=OUT_F16).view(np.float16).astype(np.float64)
-        oa = attention(qkv, seqlens, W.heads).astype(np.float32)
+        qkv = linear(codes, W.qkv.codes, W.s_qkv_in, W.qkv.s_w, W.qkv.bias, mode=OUT_F32)
+        oa = attention(qkv.astype(np.float64), seqlens, W.heads).astype(np.float32)
     W.s_o_in = act_scale(oa, hi)
     o = linear(quantize(oa, W.s_o_in, lo, hi), W.o.codes, W.s_o_in, W.o.s_w, W.o.bias)
     h1 = layernorm(o.astype(np.float64) + h, W.ln1_g, W.ln1_b).astype(np.float32)

@@ -90,7 +90,9 @@ __global__ void __launch_bounds__(kThreads) attn_i8_kernel(const Params p) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int g = lane >> 2, t = lane & 3;
     const int start = p.cu ? p.cu[b] : b * p.seq;
-    const int L = p.cu ? (p.cu[b + 1] - start) : p.seq;
+    // a sequence longer than the validated max_seq (<= kMaxL) would overrun the
+    // shared-memory tiles: clamp to max_seq (the fp16 kernels under-compute the same way)
+    const int L = min(p.cu ? (p.cu[b + 1] - start) : p.seq, p.seq);
     if (L <= 0 || (int)blockIdx.z * 64 >= L) return;
     const int Lk = (L + 31) & ~31;   // keys padded to the MMA K of P . V
     // ---- stage q, k (row-major); zero the padding rows
@@ -190,12 +192,14 @@ __global__ void __launch_bounds__(kThreads) attn_i8_kernel(const Params p) {
             bool near = false;
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                const int d = (c + i < c1) ? mx - sv[i] : 1 << 21;
+                // padded key slots (c + i >= c1) are masked by index, not by value
+                const bool valid = c + i < c1;
+                const int d = valid ? mx - sv[i] : 0;
                 const float x = __fmul_rn(c32, (float)d);
                 const float e = __fmul_rn(255.0f, __expf(-x));
                 const float r = rintf(e);
-                near |= (x <= 6.3f) && !(fabsf(fabsf(__fsub_rn(e, r)) - 0.5f) > 5e-4f);
-                pc[i] = x > 6.3f ? 0u : (uint32_t)r;
+                near |= valid && (x <= 6.3f) && !(fabsf(fabsf(__fsub_rn(e, r)) - 0.5f) > 5e-4f);
+                pc[i] = (valid && x <= 6.3f) ? (uint32_t)r : 0u;
             }
             if (near) {
 #pragma unroll 1

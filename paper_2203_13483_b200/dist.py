@@ -77,6 +77,10 @@ def gather_blocks(local: torch.Tensor, world: int, group=None) -> torch.Tensor:
     out = torch.empty((world,) + tuple(local.shape), dtype=local.dtype, device=local.device)
     if dist.get_backend(group) == "nccl":
         dist.all_gather_into_tensor(out, local.contiguous(), group=group)
+    elif local.is_cuda:   # gloo with device tensors (the multi-process tests on one GPU): staged via host
+        host = torch.empty((world,) + tuple(local.shape), dtype=local.dtype)
+        dist.all_gather(list(host.unbind(0)), local.contiguous().cpu(), group=group)
+        out.copy_(host)
     else:   # gloo (CPU tests): list form
         dist.all_gather(list(out.unbind(0)), local.contiguous(), group=group)
     return out

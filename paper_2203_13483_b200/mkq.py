@@ -6,6 +6,7 @@ CUDA device (a B200); nothing here computes on the host.
 from __future__ import annotations
 
 import ctypes
+from collections import OrderedDict
 from typing import Optional
 
 import torch
@@ -102,25 +103,33 @@ def mkq_act_scale(x: torch.Tensor, l_max: float = 7.0, p: float = 0.9999, out: O
     return out
 
 
-_TABLES = {}
+_TABLES: "OrderedDict" = OrderedDict()
+_TABLES_MAX = 64   # LRU bound: QAT / calibration loops build one table per distinct s_out
 
 
 def mkq_requant_table(gelu: bool, s_out: float, qmin: int, qmax: int, device=None, stream=None,
                       cache: bool = True) -> torch.Tensor:
     """Exact y-space lookup table of the fused (GELU +) requantize epilogue,
-    built on the device by libmkq (mkq_requant_table)."""
+    built on the device by libmkq (mkq_requant_table).  The build stream is
+    synchronized once before the table is returned, so a cached table is
+    complete for consumers on any stream."""
     device = torch.device(device if device is not None else "cuda")
     if device.index is None:
         device = torch.device("cuda", torch.cuda.current_device())
     key = (bool(gelu), float(s_out), int(qmin), int(qmax), str(device))
     if cache and key in _TABLES:
+        _TABLES.move_to_end(key)
         return _TABLES[key]
     nbytes = int(lib().mkq_requant_table_size())
     t = torch.empty(nbytes, dtype=torch.uint8, device=device)
+    st = stream if stream is not None else torch.cuda.current_stream(device)
     check("mkq_requant_table", lib().mkq_requant_table(int(gelu), float(s_out), qmin, qmax, _ptr(t), nbytes,
-                                                       _stream(stream)))
+                                                       _stream(st)))
+    st.synchronize()   # one-off: later readers on other streams see a complete table
     if cache:
         _TABLES[key] = t
+        while len(_TABLES) > _TABLES_MAX:
+            _TABLES.popitem(last=False)
     return t
 
 
@@ -219,10 +228,16 @@ def mkq_attention_i8(qkv: torch.Tensor, heads: int, batch: int, max_seq: int, s_
 def mkq_residual_layernorm(x: torch.Tensor, res: Optional[torch.Tensor], g: torch.Tensor, b: torch.Tensor,
                            eps: float = 1e-12, bits: int = 0, s_q: float = 1.0, qmin: int = -8, qmax: int = 7,
                            y: Optional[torch.Tensor] = None, q: Optional[torch.Tensor] = None, stream=None):
-    """y = LN(x + res) (post-LN, R9) [+ fused Eq.1 quantize of y]."""
+    """y = LN(x + res) (post-LN, R9) [+ fused Eq.1 quantize of y].  The C
+    call takes one leading dimension for x, res and y, so all three must
+    share x's row stride (and have unit column stride)."""
     rows, cols = x.shape
     if y is None:
-        y = torch.empty_like(x)
+        y = torch.empty_strided(x.shape, x.stride(), dtype=x.dtype, device=x.device)
+    for name, t in (("x", x), ("res", res), ("y", y)):
+        if t is not None and (t.shape != x.shape or t.stride(1) != 1 or t.stride(0) != x.stride(0)):
+            raise ValueError(f"mkq_residual_layernorm: {name} must be [{rows}, {cols}] with x's row stride "
+                             f"{x.stride(0)} and unit column stride")
     if bits and q is None:
         q = torch.empty((rows, cols // 2 if bits == 4 else cols), dtype=torch.uint8 if bits == 4 else torch.int8,
                         device=x.device)

@@ -55,12 +55,14 @@ def build_layer(params, bits: int, device="cuda", scales: Optional[Dict[str, flo
 
 
 def calibrate(layer: M.QLayer, h: torch.Tensor, batch: int, max_seq: int,
-              cu_seqlens: Optional[torch.Tensor] = None, int_attention: bool = False) -> Dict[str, float]:
+              cu_seqlens: Optional[torch.Tensor] = None, int_attention: bool = False,
+              trace: Optional[dict] = None) -> Dict[str, float]:
     """Sequential calibration of the static activation scales on a
     calibration batch, each quantization point in pipeline
     order with the scales already fixed upstream; returns and installs them.
     int_attention: also calibrate s_attn (p99.99 of |q|k|v| / 127) and run
-    the NEXT(2) integer attention core (R19)."""
+    the NEXT(2) integer attention core (R19).  trace: if a dict is given, it
+    receives the device tensor each scale was taken from (for the tests)."""
     bits, hd, F = layer.bits, layer.hidden, layer.ffn
     lo, hi = act_range(bits)
     t = layer.t
@@ -85,6 +87,8 @@ def calibrate(layer: M.QLayer, h: torch.Tensor, batch: int, max_seq: int,
     c = M.mkq_quantize_pack(h1, torch.tensor([s["s_ffn1_in"]], device=h.device), bits, lo, hi)
     g = gemm(c, t["w_1"], s["s_ffn1_in"], t["sw_1"], t["b_1"], mode=M.OUT_F32, gelu=True, K=hd)
     s["s_ffn2_in"] = act_scale(g, hi)
+    if trace is not None:
+        trace.update(h=h, qkv=qkv32 if int_attention else qkv, oa=oa, o=o, h1=h1, g=g)
     rebuilt = M.QLayer(hd, layer.heads, F, bits, layer.t, s, layer.ln_eps, use_table=layer.table is not None)
     layer.__dict__.update(rebuilt.__dict__)
     return s

@@ -61,3 +61,18 @@ def test_attention_i8_uniform_batch_and_errors():
     from paper_2203_13483_b200._lib import MkqError
     with pytest.raises(MkqError):   # sequences longer than 128 are the fp16 kernels' job
         M.mkq_attention_i8(dev(np.zeros((130, 384), np.int8)), 2, 1, 130, s, None)
+
+
+@pytest.mark.parametrize("s", [1e-3, 4e-3])
+def test_attention_i8_small_scale_ragged_keys(s):
+    """Small s_attn (c = s^2/8 tiny, so even the largest score gaps give
+    p > 0) with L % 4 != 0: the padded key slots of the last 4-key group must
+    contribute nothing (masked by index)."""
+    seqlens, heads = [1, 5, 30, 127, 66, 3], 2
+    T = sum(seqlens)
+    codes, _ = _codes(T, heads, 99, False)
+    s = np.float32(s)
+    cu = dev(np.concatenate([[0], np.cumsum(seqlens)]).astype(np.int32))
+    ref = OL.attention_int8(codes, seqlens, heads, s)
+    got = host(M.mkq_attention_i8(dev(codes), heads, len(seqlens), max(seqlens), s, cu, mode=M.OUT_F32))
+    assert np.array_equal(got.view(np.uint32), ref.view(np.uint32)), np.abs(got - ref).max()

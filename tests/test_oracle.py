@@ -462,3 +462,115 @@ def test_int_attention_bruteforce_tiny():
             num = sum(p[j] * int(c[j, 128 + t]) for j in range(L))
             y = np.float32(np.float32(num) / np.float32(sum(p)))
             assert oa[i, t] == np.float32(y * s)
+
+
+# ---------------------------------------------------------------- layer composition and calibration pins
+def _ln_textbook(x, g, b, eps=1e-12):
+    """Row LayerNorm written out with math.fsum (independent of numpy's
+    reductions): (x - mean) / sqrt(var + eps) * g + b (R9)."""
+    out = np.empty(x.shape, dtype=np.float64)
+    for r in range(x.shape[0]):
+        row = [float(v) for v in x[r]]
+        n = len(row)
+        mu = math.fsum(row) / n
+        var = math.fsum((v - mu) ** 2 for v in row) / n
+        out[r] = [(v - mu) / math.sqrt(var + eps) * float(gg) + float(bb) for v, gg, bb in zip(row, g, b)]
+    return out
+
+
+def _zero_weight_layer(hidden=128, heads=2, ffn=256, bits=4, v_identity=False):
+    """A layer whose weights are all zero (codes 0, s_w = 1e-8 floor) and whose
+    biases / LN parameters are distinct random vectors: every Linear then
+    returns its bias exactly (acc = 0 -> fma(0, sc, b) = b, R4), so each
+    intermediate of Eq.2-5 / P:93-98 has a closed form.  v_identity: W^V =
+    0.5 I instead (codes +-7 on the diagonal), so v carries the input."""
+    rng = np.random.default_rng(77)
+    z = lambda n, k: np.zeros((n, k), np.float32)  # noqa: E731
+    b = lambda n, a: rng.uniform(-a, a, n).astype(np.float32)  # noqa: E731
+    w_qkv = z(3 * hidden, hidden)
+    if v_identity:
+        w_qkv[2 * hidden:] = 0.5 * np.eye(hidden, dtype=np.float32)
+    W = OL.LayerWeights(hidden, heads, ffn, bits,
+                        OL.prepare_weight(w_qkv, b(3 * hidden, 1.0), bits),
+                        OL.prepare_weight(z(hidden, hidden), b(hidden, 1.0), bits),
+                        OL.prepare_weight(z(ffn, hidden), b(ffn, 3.0), bits),
+                        OL.prepare_weight(z(hidden, ffn), b(hidden, 1.0), bits),
+                        (1 + 0.3 * rng.standard_normal(hidden)).astype(np.float32), b(hidden, 0.5),
+                        (1 + 0.3 * rng.standard_normal(hidden)).astype(np.float32), b(hidden, 0.5))
+    return W
+
+
+def test_layer_composition_closed_form_zero_weights():
+    """bert_layer's composition (R8/R9) on a layer with zero weights:
+    q|k|v = b^{QKV}; equal keys -> OA = b^V (Eq.4-5); o = b^A; h1 = LN1(b^A + h);
+    the FFN2 input codes = Q(GELU(b^1)) (a5, a6); f = b^2; out = LN2(b^2 + h1).
+    A swapped residual (h instead of h1), a dropped bias, LN1/LN2 parameters
+    exchanged or the requant taken before GELU each fail one assertion."""
+    W = _zero_weight_layer()
+    W.s_qkv_in, W.s_o_in, W.s_ffn1_in, W.s_ffn2_in = (np.float32(v) for v in (0.5, 0.1, 0.4, 0.05))
+    seqlens = [5, 11]
+    M, d = sum(seqlens), W.hidden
+    h = synth.hidden_states(1, M, d, seed=21)
+    T = OL.bert_layer(h, W, seqlens)
+    bq = W.qkv.bias
+    assert np.array_equal(T.qkv, np.tile(bq, (M, 1)))
+    assert np.allclose(T.oa, np.tile(bq[2 * d:], (M, 1)), rtol=1e-6, atol=0)
+    assert np.array_equal(T.o, np.tile(W.o.bias, (M, 1)))
+    h1 = _ln_textbook(T.o.astype(np.float64) + h, W.ln1_g, W.ln1_b)
+    assert np.allclose(T.h1, h1, rtol=0, atol=2e-6)
+    codes = oracle.quantize(oracle.gelu_pinned(W.w1.bias)[None, :], W.s_ffn2_in, -8, 7)
+    assert np.array_equal(T.codes_ffn2_in, np.tile(codes, (M, 1)))
+    assert np.array_equal(T.f, np.tile(W.w2.bias, (M, 1)))
+    out = _ln_textbook(T.f.astype(np.float64) + T.h1, W.ln2_g, W.ln2_b)
+    assert np.allclose(T.h_out, out, rtol=0, atol=2e-6)
+    # the closed form separates the plausible mis-compositions
+    wrong = _ln_textbook(T.f.astype(np.float64) + h, W.ln2_g, W.ln2_b)
+    assert np.abs(wrong - out).max() > 1e-2
+
+
+def test_layer_attention_pools_v_within_each_sequence():
+    """With W^Q = W^K = 0 every query sees equal scores, so OA is the mean of
+    the v rows of its own sequence (Eq.4-5, R13 sequence boundaries); W^V =
+    0.5 I makes the v rows carry the (row-distinct) quantized input."""
+    W = _zero_weight_layer(v_identity=True)
+    W.s_qkv_in, W.s_o_in, W.s_ffn1_in, W.s_ffn2_in = (np.float32(v) for v in (0.5, 0.1, 0.4, 0.05))
+    seqlens = [3, 1, 12]
+    M, d = sum(seqlens), W.hidden
+    h = synth.hidden_states(1, M, d, seed=22)
+    T = OL.bert_layer(h, W, seqlens)
+    v = T.qkv[:, 2 * d:].astype(np.float64)
+    assert np.abs(v - v[0]).max() > 0.1           # rows differ: pooling is observable
+    r0 = 0
+    for L in seqlens:
+        ref = v[r0:r0 + L].mean(axis=0)
+        assert np.allclose(T.oa[r0:r0 + L], np.tile(ref, (L, 1)), rtol=1e-6, atol=1e-7)
+        r0 += L
+
+
+@pytest.mark.parametrize("int_attention", [False, True])
+def test_calibrate_takes_each_scale_from_its_own_intermediate(int_attention):
+    """OL.calibrate (P:72 'top 0.01%', R6; pipeline order P:121) on the
+    zero-weight layer: s_qkv_in from h, s_attn from q|k|v = b^{QKV} (/127),
+    s_o_in from OA = b^V, s_ffn1_in from LN1(b^A + h), s_ffn2_in from
+    GELU(b^1) -- not from b^1 (pre-GELU) or from h1."""
+    W = _zero_weight_layer()
+    seqlens = [16, 16]
+    M, d = sum(seqlens), W.hidden
+    hc = synth.hidden_states(1, M, d, seed=1000000)
+    OL.calibrate(hc, W, seqlens, int_attention=int_attention)
+    tile = lambda v: np.tile(v, (M, 1))  # noqa: E731
+    assert W.s_qkv_in == oracle.act_scale(hc, 7)
+    bq = W.qkv.bias
+    if int_attention:
+        assert W.s_attn == oracle.act_scale(tile(bq), 127)
+        # OA of the int8 core on identical keys is the exact mean of the v codes
+        cv = oracle.quantize(bq[None, 2 * d:], W.s_attn, -127, 127)[0].astype(np.float32)
+        oa = (cv * np.float32(W.s_attn)).astype(np.float32)
+        assert np.isclose(W.s_o_in, oracle.act_scale(tile(oa), 7), rtol=1e-6)
+    else:
+        assert np.isclose(W.s_o_in, oracle.act_scale(tile(bq[2 * d:]), 7), rtol=1e-6)
+    h1 = _ln_textbook(tile(W.o.bias).astype(np.float64) + hc, W.ln1_g, W.ln1_b)
+    assert np.isclose(W.s_ffn1_in, oracle.act_scale(h1, 7), rtol=1e-6)
+    g = tile(oracle.gelu_pinned(W.w1.bias))
+    assert W.s_ffn2_in == oracle.act_scale(g, 7)
+    assert W.s_ffn2_in != oracle.act_scale(tile(W.w1.bias), 7)
