@@ -59,7 +59,10 @@ struct Gemm2Cfg {
     // (sc, b) per column: 2 tile buffers x BN (shared by the epilogue), or
     // (kLut4) one private kColsPerWarp slice per epilogue warp
     static constexpr int kScb = kLut4 ? kEpiWarps * kColsPerWarp * 8 : 2 * BN * 8;
-    static constexpr int kStagePerWarp = kLut4 ? 512 : 2048;   // 32 rows x 16 B (int4) / 64 B output block per warp
+    // per epilogue warp: kLut4 one or (8 warps) two 32 x 16 B int4 blocks
+    // (double-buffered TMA stores), else one 32 x 64 B output block
+    static constexpr int kStgBufs = kLut4 && EPI_ <= 8 ? 2 : 1;
+    static constexpr int kStagePerWarp = kLut4 ? 512 * kStgBufs : 2048;
     static constexpr int kStaging = kEpiWarps * kStagePerWarp;
     static constexpr int kTabBytes = kLut4 ? (int)rq::kSmem4Bytes : (int)rq::kSmemBytes;
     // kLut4 register split (setmaxnreg; must fit the launch allocation)
@@ -275,69 +278,97 @@ __device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {   // two 
     return *reinterpret_cast<float2*>(&r);
 }
 
+// A register the compiler cannot prove warp-uniform or constant: keeps values
+// used by every output in one vector register (a uniform value feeding an FFMA
+// that already takes a uniform operand is otherwise re-copied per use, and a
+// folded constant is re-added per use).
+__device__ __forceinline__ uint32_t lane_reg(uint32_t x) {
+    uint32_t r;
+    asm volatile("shfl.sync.idx.b32 %0, %1, %2, 0x1f, 0xffffffff;" : "=r"(r) : "r"(x), "r"(threadIdx.x & 31));
+    return r;
+}
+
 // 32 int4 requantized codes of one accumulator row (columns cl..cl+31) through
 // the compact table (requant.cuh, "compact int4 table"): per output one cell
-// computation, one conflict-free 32-bit lookup (tab = this lane's replica),
-// one fp32 compare and a nibble insert; lanes within 511 ulps of a threshold
-// word, or any lane when the table is unusable, are evaluated directly.
-// scb: (sc, sc', b, b') per column pair, so the dequant fma runs as f32x2.
+// computation, one conflict-free 32-bit lookup (tabm = this lane's replica
+// minus the cell bias), one fp32 compare and a byte gather; outputs within the
+// threshold word's direct-evaluation window (rq::kWin4), or all outputs when
+// the table is unusable, are evaluated directly.  scb: (sc, sc', b, b') per
+// column pair (f32x2 dequant).  Per output about 10 instructions: I2F, 1/2
+// FFMA2 + 1/2 LDS.128 (dequant), FFMA.SAT + 1/2 FFMA2 + IMAD (cell address),
+// LDS, IADD3 + 1/2 VIMNMX3 (window), FSETP + SHF (decision), 1 PRMT/LOP3
+// (nibble packing).
 template <bool kFold>
-__device__ __forceinline__ void epi_lut4(const EpiParams& ep, const uint32_t (&v)[32], uint32_t scb, uint32_t tab,
+__device__ __forceinline__ void epi_lut4(const EpiParams& ep, const uint32_t (&v)[32], uint32_t scb, uint32_t tabm,
                                          float a4, float b4, bool tvalid, uint32_t (&w)[4]) {
-    uint32_t bad = tvalid ? 0xFFFFFFFFu : 0u;
-    const uint32_t tabm = tab - (rq::kMagic << 7);   // (bits - magic) * 128 + tab, mod 2^32
-    // phase 1: y for all 32 outputs (dequant as f32x2), phase 2: all 32 cell
-    // addresses and table loads in flight, phase 3: the decisions
-    float y[32];
+    // Two halves of 16 outputs (bounds the live registers: v[32] + y[16] + e[16]):
+    // phase 1 y (dequant as f32x2), phase 2 all 16 cell addresses and table
+    // loads in flight, phase 3 the decisions, the (rare, warp-uniform) direct
+    // evaluation of window lanes while y is still live, the byte gather.
 #pragma unroll
-    for (int i = 0; i < 32; i += 2) {
-        const float4 sb = lds128f(scb + 8u * (uint32_t)i);
-        const int32_t a0 = kFold ? (int32_t)v[i] : ((int32_t)v[i] >> 8);
-        const int32_t a1 = kFold ? (int32_t)v[i + 1] : ((int32_t)v[i + 1] >> 8);
-        const float2 yy = fma2(make_float2(__int2float_rn(a0), __int2float_rn(a1)), make_float2(sb.x, sb.y),
-                               make_float2(sb.z, sb.w));
-        y[i] = yy.x;
-        y[i + 1] = yy.y;
-    }
-    uint32_t e[32];
+    for (int hh = 0; hh < 2; ++hh) {
+        float y[16];
 #pragma unroll
-    for (int i = 0; i < 32; i += 2) {
-        const float2 cf = fma2(make_float2(rq::fma_sat(y[i], a4, b4), rq::fma_sat(y[i + 1], a4, b4)),
-                               make_float2(255.0f, 255.0f), make_float2(8388608.0f, 8388608.0f));
-        e[i] = __float_as_uint(cf.x) * 128u + tabm;
-        e[i + 1] = __float_as_uint(cf.y) * 128u + tabm;
-    }
+        for (int i = 0; i < 16; i += 2) {
+            const float4 sb = lds128f(scb + 8u * (uint32_t)(16 * hh + i));
+            const int32_t a0 = kFold ? (int32_t)v[16 * hh + i] : ((int32_t)v[16 * hh + i] >> 8);
+            const int32_t a1 = kFold ? (int32_t)v[16 * hh + i + 1] : ((int32_t)v[16 * hh + i + 1] >> 8);
+            const float2 yy = fma2(make_float2(__int2float_rn(a0), __int2float_rn(a1)), make_float2(sb.x, sb.y),
+                                   make_float2(sb.z, sb.w));
+            y[i] = yy.x;
+            y[i + 1] = yy.y;
+        }
+        uint32_t e[16];
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
+        for (int i = 0; i < 16; i += 2) {
+            const float2 cf = fma2(make_float2(rq::fma_sat(y[i], a4, b4), rq::fma_sat(y[i + 1], a4, b4)),
+                                   make_float2(255.0f, 255.0f), make_float2(8388608.0f, 8388608.0f));
+            e[i] = __float_as_uint(cf.x) * 128u + tabm;
+            e[i + 1] = __float_as_uint(cf.y) * 128u + tabm;
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
 #ifdef MKQ_ABL_L4NOLUT   // ablation (diagnostics only)
-        e[i] = e[i] * 0x01010101u;
+            e[i] = e[i] * 0x01010101u;
 #else
-        e[i] = lds32(e[i]);
+            e[i] = lds32(e[i]);
 #endif
-    }
+        }
+        uint32_t bad = tvalid ? 0xFFFFFFFFu : 0u;
 #pragma unroll
-    for (int ii = 0; ii < 32; ++ii) {
-        bad = min(bad, __float_as_uint(y[ii]) - e[ii] + 511u);
-        const uint32_t f = y[ii] >= __uint_as_float(e[ii]) ? (e[ii] >> 4) : e[ii];
-        const int k = ii & 7;
-        if (k == 0)
-            w[ii >> 3] = f & 0xFu;
-        else
-            w[ii >> 3] |= (f << (4 * k)) & (0xFu << (4 * k));
-    }
-    if (__builtin_expect(__any_sync(0xffffffffu, bad < 1023u), 0)) {
+        for (int ii = 0; ii < 16; ++ii) {
+            bad = min(bad, __float_as_uint(y[ii]) - e[ii] + rq::kWin4);
+            e[ii] = y[ii] >= __uint_as_float(e[ii]) ? (e[ii] >> 4) : e[ii];   // code in the low nibble
+        }
+        if (__builtin_expect(__any_sync(0xffffffffu, bad < 2u * rq::kWin4 + 1u), 0)) {
+            // mask of this lane's window outputs, then one call site in a loop
+            // over the set bits (register selects, no local-memory indexing)
+            uint32_t nm = 0;
 #pragma unroll
-        for (int ii = 0; ii < 32; ++ii) {
-            const uint32_t pb = scb + 16u * (uint32_t)(ii >> 1) + 4u * (uint32_t)(ii & 1);
-            const float sc = __uint_as_float(lds32(pb)), bb = __uint_as_float(lds32(pb + 8u));
-            const int32_t acc = kFold ? (int32_t)v[ii] : ((int32_t)v[ii] >> 8);
-            const float y = __fmaf_rn(__int2float_rn(acc), sc, bb);
-            const uint32_t e = lds32(tab + (rq::cell4(y, a4, b4) << 7));
-            if (!tvalid || __float_as_uint(y) - e + 511u < 1023u) {
-                const uint32_t c = (uint32_t)requant_direct(y, ep.gelu, ep.s_out, ep.qmin, ep.qmax) & 0xFu;
-                const int k = ii & 7;
-                w[ii >> 3] = (w[ii >> 3] & ~(0xFu << (4 * k))) | (c << (4 * k));
+            for (int ii = 0; ii < 16; ++ii) {
+                const uint32_t ew = lds32(tabm + __float_as_uint(__fmaf_rn(rq::fma_sat(y[ii], a4, b4), 255.0f,
+                                                                           8388608.0f)) * 128u);
+                if (!tvalid || __float_as_uint(y[ii]) - ew + rq::kWin4 < 2u * rq::kWin4 + 1u) nm |= 1u << ii;
             }
+            while (nm) {
+                const int i = __ffs(nm) - 1;
+                nm &= nm - 1;
+                float yv = y[0];
+#pragma unroll
+                for (int k = 1; k < 16; ++k) yv = k == i ? y[k] : yv;
+                const uint32_t c = (uint32_t)requant_direct(yv, ep.gelu, ep.s_out, ep.qmin, ep.qmax);
+#pragma unroll
+                for (int k = 0; k < 16; ++k) e[k] = k == i ? c : e[k];
+            }
+        }
+        // nibble packing: bytes of the even / odd codes gathered with PRMT, then
+        // w = (even & 0x0F0F0F0F) | ((odd << 4) & 0xF0F0F0F0) in one LOP3
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {
+            const uint32_t* f = e + 8 * g;
+            const uint32_t ev = __byte_perm(__byte_perm(f[0], f[2], 0x0040), __byte_perm(f[4], f[6], 0x0040), 0x5410);
+            const uint32_t od = __byte_perm(__byte_perm(f[1], f[3], 0x0040), __byte_perm(f[5], f[7], 0x0040), 0x5410);
+            w[2 * hh + g] = (ev & 0x0F0F0F0Fu) | ((od << 4) & 0xF0F0F0F0u);
         }
     }
 }
@@ -518,6 +549,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
             }
         };
         if constexpr (Cfg::kLut4) load_scales(cluster);
+        // this lane's replica of the compact table, and the same minus the cell
+        // bias (bits(2^23) * 128 = 2^31 mod 2^32), held in vector registers
+        const uint32_t tab = ptx::smem_u32(th) + 4u * (uint32_t)lane;
+        const uint32_t tabm = lane_reg(tab - (rq::kMagic << 7));
+        a4 = __uint_as_float(lane_reg(__float_as_uint(a4)));
         int it = 0;
         for (int tile = cluster; tile < num_tiles; tile += nclusters, ++it) {
             const int m0 = (tile / n_tiles) * 2 * BM + (int)rank * BM;
@@ -549,45 +585,72 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
                 __syncwarp();
                 load_scales(tile + nclusters);   // in flight during this tile
                 GTRACE(2);
-                MKQ_WAIT_SLEEP(128, &tfull[ab], aph);
+                // Accumulator wait.  Default: every warp sleeps between polls
+                // (test_wait + nanosleep): the suspend-hint try_wait wakes on every
+                // barrier event of the CTA, and sixteen epilogue warps polling with
+                // it spun through ~20% of the SM's issue slots (r02 profile).
+                // MKQ_EPI_ONE_POLLER: one warp polls, the rest block on a named
+                // barrier (this phase-locks the warps' TMEM reads at the tile start).
+#ifdef MKQ_EPI_ONE_POLLER
+                if (e == 0) ptx::mbar_wait(&tfull[ab], aph);
+                ptx::named_bar_sync(2, kEpiThreads);
+#else
+                ptx::mbar_wait_sleep<64>(&tfull[ab], aph);
+#endif
                 GTRACE(3);
                 ptx::tc_fence_after();
                 const int row0 = m0 + q * 32;
-                const uint32_t tab = ptx::smem_u32(th) + 4u * (uint32_t)lane;
-#pragma unroll 1
-                for (int j = 0; j < Cfg::kColsPerWarp / 32; ++j) {
-                    const int cl = h * Cfg::kColsPerWarp + 32 * j;
-                    const int n = n0 + cl;
-                    if (n >= N) break;
-#ifdef MKQ_ABL_NOEPI
-                    break;
-#endif
-                    GTRACE(4);
-                    uint32_t v[32];
-                    ptx::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + ab * BN + cl, v);
-                    ptx::tmem_ld_wait();
+                constexpr int kCh = Cfg::kColsPerWarp / 32;
+                const uint32_t tb = tmem_base + ((uint32_t)(q * 32) << 16) + ab * BN + h * Cfg::kColsPerWarp;
+                // TMEM readback one chunk ahead (tcgen05.ld of chunk j+1 in flight
+                // while chunk j is computed; wait::ld covers all of a thread's loads,
+                // so it is issued after chunk j's work) when the registers allow it
+                constexpr bool kPrefetch = Cfg::kRegEpi >= 160;
+                uint32_t va[32], vb[32];
+                ptx::tmem_ld_32x32b_x32(tb, va);
+                ptx::tmem_ld_wait_regs(va);
+                auto chunk = [&](int j, uint32_t (&cur)[32], uint32_t (&nxt)[32]) {
+                    if (kPrefetch && j + 1 < kCh) ptx::tmem_ld_32x32b_x32(tb + 32 * (j + 1), nxt);
+                    const int n = n0 + h * Cfg::kColsPerWarp + 32 * j;
                     GTRACE(5);
                     uint32_t w[4];
                     const uint32_t sba = ptx::smem_u32(wsb + 32 * j);
-                    if (wfold)
-                        epi_lut4<true>(ep, v, sba, tab, a4, b4, use_table, w);
-                    else
-                        epi_lut4<false>(ep, v, sba, tab, a4, b4, use_table, w);
+                    // unfolded tile (a column scale too small to absorb the 2^-8;
+                    // rare): shift the accumulators here, so one copy of the
+                    // epilogue code serves both (scb then holds the plain sc)
+                    if (__builtin_expect(!wfold, 0)) {
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) cur[i] = (uint32_t)((int32_t)cur[i] >> 8);
+                    }
+                    epi_lut4<true>(ep, cur, sba, tabm, a4, b4, use_table, w);
                     GTRACE(6);
-                    // the previous chunk's TMA store must have read the staging block
-                    // (issued a whole chunk of work ago)
-                    if (lane == 0) ptx::tma_store_wait_read<0>();
+                    // staging block(s): the store that last used this block must
+                    // have read it
+                    uint8_t* stg = stage + 512 * (j % Cfg::kStgBufs);
+                    if (lane == 0) ptx::tma_store_wait_read<Cfg::kStgBufs - 1>();
                     __syncwarp();
-                    *reinterpret_cast<uint4*>(stage + lane * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+                    *reinterpret_cast<uint4*>(stg + lane * 16) = make_uint4(w[0], w[1], w[2], w[3]);
                     ptx::fence_proxy_async_smem();
                     __syncwarp();
 #ifndef MKQ_ABL_L4NOSTORE
-                    if (lane == 0) {
-                        ptx::tma_store_2d(&tmO, stage, n / 2, row0);
+                    if (lane == 0 && n < N) {
+                        ptx::tma_store_2d(&tmO, stg, n / 2, row0);
                         ptx::tma_store_commit();
                     }
 #endif
+                    if (j + 1 < kCh) {
+                        if (!kPrefetch) ptx::tmem_ld_32x32b_x32(tb + 32 * (j + 1), nxt);
+                        ptx::tmem_ld_wait_regs(nxt);
+                    }
+                };
+                static_assert(kCh % 2 == 0, "chunk pairs");
+#ifndef MKQ_ABL_NOEPI
+#pragma unroll 1
+                for (int j = 0; j < kCh; j += 2) {
+                    chunk(j, va, vb);
+                    chunk(j + 1, vb, va);
                 }
+#endif
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive_remote(ptx::mapa(&tempty[ab], 0));
@@ -607,8 +670,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
             // fold the >> 8 into sc unless some column's sc is too small (rare; tile-uniform)
             const bool fold = !ptx::named_bar_sync_or(1, kEpiThreads, tiny);
             if (et < BN) sb[et] = make_float2(fold ? __fmul_rn(sc, 0x1p-8f) : sc, bn);
+            if (e == 0) MKQ_WAIT_SLEEP(128, &tfull[ab], aph);   // one poller (see the kLut4 path)
             ptx::named_bar_sync(1, kEpiThreads);
-            MKQ_WAIT_SLEEP(128, &tfull[ab], aph);
             ptx::tc_fence_after();
             const int row0 = m0 + q * 32;
             {

@@ -464,8 +464,12 @@ mkq_status gemm_common(bool int4, const void* a, int64_t lda, const void* w, int
         static const bool no_lut4 = getenv("MKQ_NO_LUT4") != nullptr;   // diagnostics
         if (N % 256 == 0) {
             // (8 unpack warps with 88-register epilogue warps measured 7% slower)
-            if (many_epi && e.out == MKQ_OUT_I4 && p2.table && !no_lut4)
+            static const int lut4_epi = [] { const char* v = getenv("MKQ_LUT4_EPI"); return v ? atoi(v) : 16; }();
+            if (many_epi && e.out == MKQ_OUT_I4 && p2.table && !no_lut4) {
+                if (lut4_epi == 8)
+                    return launch_gemm2<mkq::Gemm2Cfg<256, 8, 4, true>>(a, lda, w, ldw, (int)M, (int)N, (int)K, p2, sms, st);
                 return launch_gemm2<mkq::Gemm2Cfg<256, 16, 4, true>>(a, lda, w, ldw, (int)M, (int)N, (int)K, p2, sms, st);
+            }
             if (many_epi)
                 return launch_gemm2<mkq::Gemm2Cfg<256, 16, 4>>(a, lda, w, ldw, (int)M, (int)N, (int)K, p2, sms, st);
             return launch_gemm2<mkq::Gemm2Cfg<256>>(a, lda, w, ldw, (int)M, (int)N, (int)K, p2, sms, st);

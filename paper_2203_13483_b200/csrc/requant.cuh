@@ -46,13 +46,15 @@ struct Change {
 // ---- compact int4 table (the FFN1 epilogue's fast path; int4 outputs only)
 // 256 cells over the span of the change points, one 32-bit word per cell:
 //     cell(y) = RN(255 * sat(fma(y, a, b)))  in [0, 255]   (cell4 below)
-//     word    = (bits(thr) & ~0x1FF) | below | above << 4            (>= 1 change)
+//     word    = (bits(thr) & ~0xFF) | below | above << 4             (>= 1 change)
 //             = 0x7F800000 | below | below << 4  (NaN: y >= it is false)  (none)
-// The low 9 bits of the threshold are given up for the two nibbles, so the
-// fp32 compare  y >= float(word)  decides exactly except for y within 511 ulps
-// of the word; the epilogue detects those lanes with one integer test
-// (bits(y) - word + 511 < 1023, unsigned) and evaluates them directly.  A
-// table needing two change points in one cell is marked invalid.  In shared
+// The low 8 bits of the threshold are given up for the two nibbles: every
+// change point of the cell lies in W = {bits in [word & ~0xFF, +256)}, a run of
+// 256 consecutive floats, so the fp32 compare  y >= float(word)  decides
+// exactly for y outside W; the epilogue detects the lanes of the superset
+// window  bits(y) - word + kWin4 < 2 kWin4 + 1  (unsigned, kWin4 = 255) with
+// one integer test and evaluates them directly.  A cell whose change points
+// do not fit one W makes the table invalid.  In shared
 // memory each word is replicated 32 times (lane l reads bank l), so a warp's
 // 32 lookups are one conflict-free wavefront.
 constexpr int kCells4 = 256;
@@ -79,10 +81,11 @@ constexpr uint32_t kMagic = 0x4B000000u;   // bits of 2^23
 __device__ __forceinline__ uint32_t cell4(float y, float a, float b) {
     return __float_as_uint(__fmaf_rn(fma_sat(y, a, b), 255.0f, 8388608.0f)) - kMagic;
 }
-// 0 = decided: *code = the int4 field; 1 = y is within 511 ulps of the
-// cell's threshold word (evaluate directly)
+// 0 = decided: *code = the int4 field; 1 = y is in the cell's direct-
+// evaluation window (within kWin4 ulps of the threshold word)
+constexpr uint32_t kWin4 = 255u;
 __device__ __forceinline__ bool lookup4(uint32_t w, float y, uint32_t* field) {
-    if (__float_as_uint(y) - w + 511u < 1023u) return true;
+    if (__float_as_uint(y) - w + kWin4 < 2u * kWin4 + 1u) return true;
     *field = (y >= __uint_as_float(w) ? (w >> 4) : w) & 0xFu;
     return false;
 }
@@ -228,10 +231,10 @@ __global__ void finalize4_kernel(Header* h, Header4* h4, uint32_t* cells4, const
     // A cell may hold a cluster of change points (gelu_pinned(y)/s is not
     // monotone at the ulp level, so a code can flicker c, c+1, c, c+1 over a
     // few floats): one word covers it when every point of the cluster lies in
-    // the word's +-511-ulp window, where the epilogue evaluates directly;
-    // below / above the window the codes are the cluster's first "before"
+    // the word's 256-float run W (see above), where the epilogue evaluates
+    // directly; below / above W the codes are the cluster's first "before"
     // and last "after" (the verify pass re-checks every float).
-    auto in_win = [](uint32_t b, uint32_t wb) { return b - wb + 511u < 1023u; };
+    auto in_win = [](uint32_t b, uint32_t wb) { return b - wb < 256u; };
     for (int i = 0; i < kCells4 && ok; ++i) {
         uint32_t w = 0x7F800000u | (uint32_t)(run & 0xF) * 0x11u;
         const int before = run;
@@ -246,8 +249,8 @@ __global__ void finalize4_kernel(Header* h, Header4* h4, uint32_t* cells4, const
             ++p;
         }
         if (cnt >= 1) {
-            uint32_t wb = fb & ~0x1FFu;
-            if (!(in_win(fb, wb) && in_win(lb, wb))) wb = lb & ~0x1FFu;
+            uint32_t wb = fb & ~0xFFu;
+            if (!(in_win(fb, wb) && in_win(lb, wb))) wb = lb & ~0xFFu;
             if (!(in_win(fb, wb) && in_win(lb, wb))) ok = false;
             w = wb | (uint32_t)(before & 0xF) | ((uint32_t)(run & 0xF) << 4);
         }

@@ -26,7 +26,7 @@ def main():
     h_in = torch.from_numpy(synth.hidden_states(B, S, hd, seed=0)).to(dev)
     ws = torch.empty(L.workspace_size(T), dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
-    calls, _ = bench.stage_calls(M, L, h_in, ws, T, stream)
+    calls, _ = bench.stage_calls(M, L, h_in, B, T, stream)
     for c in calls:
         c[1]()
     torch.cuda.synchronize()
