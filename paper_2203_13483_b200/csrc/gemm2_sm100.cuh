@@ -288,6 +288,13 @@ __device__ __forceinline__ uint32_t lane_reg(uint32_t x) {
     return r;
 }
 
+// a - b as an IMAD (FMA pipe; the epilogue is bound by the ALU pipe)
+__device__ __forceinline__ uint32_t sub_fma(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("mad.lo.u32 %0, %1, 0xFFFFFFFF, %2;" : "=r"(r) : "r"(b), "r"(a));
+    return r;
+}
+
 // 32 int4 requantized codes of one accumulator row (columns cl..cl+31) through
 // the compact table (requant.cuh, "compact int4 table"): per output one cell
 // computation, one conflict-free 32-bit lookup (tabm = this lane's replica
@@ -296,7 +303,7 @@ __device__ __forceinline__ uint32_t lane_reg(uint32_t x) {
 // the table is unusable, are evaluated directly.  scb: (sc, sc', b, b') per
 // column pair (f32x2 dequant).  Per output about 10 instructions: I2F, 1/2
 // FFMA2 + 1/2 LDS.128 (dequant), FFMA.SAT + 1/2 FFMA2 + IMAD (cell address),
-// LDS, IADD3 + 1/2 VIMNMX3 (window), FSETP + SHF (decision), 1 PRMT/LOP3
+// LDS, IMAD + 1/2 VIMNMX3 (window), FSETP + SHF (decision), 1 PRMT/LOP3
 // (nibble packing).
 template <bool kFold>
 __device__ __forceinline__ void epi_lut4(const EpiParams& ep, const uint32_t (&v)[32], uint32_t scb, uint32_t tabm,
@@ -337,10 +344,10 @@ __device__ __forceinline__ void epi_lut4(const EpiParams& ep, const uint32_t (&v
         uint32_t bad = tvalid ? 0xFFFFFFFFu : 0u;
 #pragma unroll
         for (int ii = 0; ii < 16; ++ii) {
-            bad = min(bad, __float_as_uint(y[ii]) - e[ii] + rq::kWin4);
+            bad = min(bad, sub_fma(__float_as_uint(y[ii]), e[ii]));   // bits(y) - word (rq::kWin4 window)
             e[ii] = y[ii] >= __uint_as_float(e[ii]) ? (e[ii] >> 4) : e[ii];   // code in the low nibble
         }
-        if (__builtin_expect(__any_sync(0xffffffffu, bad < 2u * rq::kWin4 + 1u), 0)) {
+        if (__builtin_expect(__any_sync(0xffffffffu, bad < rq::kWin4), 0)) {
             // mask of this lane's window outputs, then one call site in a loop
             // over the set bits (register selects, no local-memory indexing)
             uint32_t nm = 0;
@@ -348,7 +355,7 @@ __device__ __forceinline__ void epi_lut4(const EpiParams& ep, const uint32_t (&v
             for (int ii = 0; ii < 16; ++ii) {
                 const uint32_t ew = lds32(tabm + __float_as_uint(__fmaf_rn(rq::fma_sat(y[ii], a4, b4), 255.0f,
                                                                            8388608.0f)) * 128u);
-                if (!tvalid || __float_as_uint(y[ii]) - ew + rq::kWin4 < 2u * rq::kWin4 + 1u) nm |= 1u << ii;
+                if (!tvalid || __float_as_uint(y[ii]) - ew < rq::kWin4) nm |= 1u << ii;
             }
             while (nm) {
                 const int i = __ffs(nm) - 1;
@@ -594,6 +601,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
 #ifdef MKQ_EPI_ONE_POLLER
                 if (e == 0) ptx::mbar_wait(&tfull[ab], aph);
                 ptx::named_bar_sync(2, kEpiThreads);
+#elif defined(MKQ_EPI_WAIT_NS)
+#if MKQ_EPI_WAIT_NS == 0
+                ptx::mbar_wait(&tfull[ab], aph);
+#else
+                ptx::mbar_wait_sleep<MKQ_EPI_WAIT_NS>(&tfull[ab], aph);
+#endif
 #else
                 ptx::mbar_wait_sleep<64>(&tfull[ab], aph);
 #endif
@@ -670,8 +683,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
             // fold the >> 8 into sc unless some column's sc is too small (rare; tile-uniform)
             const bool fold = !ptx::named_bar_sync_or(1, kEpiThreads, tiny);
             if (et < BN) sb[et] = make_float2(fold ? __fmul_rn(sc, 0x1p-8f) : sc, bn);
-            if (e == 0) MKQ_WAIT_SLEEP(128, &tfull[ab], aph);   // one poller (see the kLut4 path)
             ptx::named_bar_sync(1, kEpiThreads);
+            MKQ_WAIT_SLEEP(128, &tfull[ab], aph);
             ptx::tc_fence_after();
             const int row0 = m0 + q * 32;
             {
@@ -745,10 +758,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
                 for (int i = 0; i < kPer; ++i) {
                     const uint4 pv = pk[i];
                     uint4 lo, hi;
-                    lo.x = (pv.x * 16u) & 0xF0F0F0F0u; hi.x = pv.x & 0xF0F0F0F0u;
-                    lo.y = (pv.y * 16u) & 0xF0F0F0F0u; hi.y = pv.y & 0xF0F0F0F0u;
-                    lo.z = (pv.z * 16u) & 0xF0F0F0F0u; hi.z = pv.z & 0xF0F0F0F0u;
-                    lo.w = (pv.w * 16u) & 0xF0F0F0F0u; hi.w = pv.w & 0xF0F0F0F0u;
+                    ptx::unpack_i4x8(pv.x, lo.x, hi.x);
+                    ptx::unpack_i4x8(pv.y, lo.y, hi.y);
+                    ptx::unpack_i4x8(pv.z, lo.z, hi.z);
+                    ptx::unpack_i4x8(pv.w, lo.w, hi.w);
                     const uint32_t rb = dst + (uint32_t)i * (kRowsPerPass * 128u);
                     ptx::sts128(rb + dlo_off, lo);
                     ptx::sts128(rb + dhi_off, hi);

@@ -88,6 +88,18 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
     while (!mbar_test(bar, parity)) __nanosleep(kNs);
 }
 
+// ------------------------------------------------------------------ int4 unpack
+// One packed word (8 int4 codes, element k in nibble k) -> two int8 words:
+// lo = 16 x the even codes, hi = 16 x the odd codes (the even/odd permutation
+// both GEMM operands share).  L = p & 0x0F0F0F0F on the ALU pipe; lo = 16 L and
+// hi = p - L as IMADs on the FMA pipe (the unpack warps share the ALU pipe
+// with the ALU-heavy epilogue; (p << 4) & M and p & M would be 2 ALU ops + 1).
+__device__ __forceinline__ void unpack_i4x8(uint32_t p, uint32_t& lo, uint32_t& hi) {
+    const uint32_t l = p & 0x0F0F0F0Fu;
+    asm("mad.lo.u32 %0, %1, 16, 0;" : "=r"(lo) : "r"(l));
+    asm("mad.lo.u32 %0, %1, 0xFFFFFFFF, %2;" : "=r"(hi) : "r"(l), "r"(p));
+}
+
 // ------------------------------------------------------------------ fences
 // Generic-proxy writes to shared memory -> visible to the async proxy
 // (tensor core / TMA reads).  Executed by every writing thread.

@@ -46,15 +46,17 @@ struct Change {
 // ---- compact int4 table (the FFN1 epilogue's fast path; int4 outputs only)
 // 256 cells over the span of the change points, one 32-bit word per cell:
 //     cell(y) = RN(255 * sat(fma(y, a, b)))  in [0, 255]   (cell4 below)
-//     word    = (bits(thr) & ~0xFF) | below | above << 4             (>= 1 change)
+//     word    = (F - 256) | below | above << 4                      (>= 1 change)
 //             = 0x7F800000 | below | below << 4  (NaN: y >= it is false)  (none)
-// The low 8 bits of the threshold are given up for the two nibbles: every
-// change point of the cell lies in W = {bits in [word & ~0xFF, +256)}, a run of
-// 256 consecutive floats, so the fp32 compare  y >= float(word)  decides
-// exactly for y outside W; the epilogue detects the lanes of the superset
-// window  bits(y) - word + kWin4 < 2 kWin4 + 1  (unsigned, kWin4 = 255) with
-// one integer test and evaluates them directly.  A cell whose change points
-// do not fit one W makes the table invalid.  In shared
+// where every change point of the cell lies in the 256-float run
+// R = {bits in [F, F + 256)}, F a multiple of 256.  The word sits just below
+// R (in magnitude), so the window  D = {bits(y) - word < kWin4}  (unsigned,
+// kWin4 = 512: bits in [word, word + 512) >= [F - 1, F + 256)) contains R, and
+// outside D the fp32 compare  y >= float(word)  decides exactly (above R or
+// below R, for either sign of the threshold).  The epilogue computes
+// bits(y) - word with one IMAD (FMA pipe) and evaluates the lanes in D
+// directly.  A cell whose change points do not fit one R makes the table
+// invalid.  In shared
 // memory each word is replicated 32 times (lane l reads bank l), so a warp's
 // 32 lookups are one conflict-free wavefront.
 constexpr int kCells4 = 256;
@@ -82,10 +84,10 @@ __device__ __forceinline__ uint32_t cell4(float y, float a, float b) {
     return __float_as_uint(__fmaf_rn(fma_sat(y, a, b), 255.0f, 8388608.0f)) - kMagic;
 }
 // 0 = decided: *code = the int4 field; 1 = y is in the cell's direct-
-// evaluation window (within kWin4 ulps of the threshold word)
-constexpr uint32_t kWin4 = 255u;
+// evaluation window D (the kWin4 floats from the threshold word up in magnitude)
+constexpr uint32_t kWin4 = 512u;
 __device__ __forceinline__ bool lookup4(uint32_t w, float y, uint32_t* field) {
-    if (__float_as_uint(y) - w + kWin4 < 2u * kWin4 + 1u) return true;
+    if (__float_as_uint(y) - w < kWin4) return true;
     *field = (y >= __uint_as_float(w) ? (w >> 4) : w) & 0xFu;
     return false;
 }
@@ -231,8 +233,8 @@ __global__ void finalize4_kernel(Header* h, Header4* h4, uint32_t* cells4, const
     // A cell may hold a cluster of change points (gelu_pinned(y)/s is not
     // monotone at the ulp level, so a code can flicker c, c+1, c, c+1 over a
     // few floats): one word covers it when every point of the cluster lies in
-    // the word's 256-float run W (see above), where the epilogue evaluates
-    // directly; below / above W the codes are the cluster's first "before"
+    // one 256-float run R (see above), where the epilogue evaluates
+    // directly; below / above R the codes are the cluster's first "before"
     // and last "after" (the verify pass re-checks every float).
     auto in_win = [](uint32_t b, uint32_t wb) { return b - wb < 256u; };
     for (int i = 0; i < kCells4 && ok; ++i) {
@@ -252,7 +254,8 @@ __global__ void finalize4_kernel(Header* h, Header4* h4, uint32_t* cells4, const
             uint32_t wb = fb & ~0xFFu;
             if (!(in_win(fb, wb) && in_win(lb, wb))) wb = lb & ~0xFFu;
             if (!(in_win(fb, wb) && in_win(lb, wb))) ok = false;
-            w = wb | (uint32_t)(before & 0xF) | ((uint32_t)(run & 0xF) << 4);
+            if ((wb & 0x7FFFFFFFu) < 256u) ok = false;   // F - 256 would cross zero (denormal thresholds)
+            w = (wb - 256u) | (uint32_t)(before & 0xF) | ((uint32_t)(run & 0xF) << 4);
         }
         cells4[i] = w;
     }

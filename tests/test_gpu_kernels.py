@@ -360,7 +360,7 @@ TAB4 = 64 + 1024 * 8   # byte offset of the compact int4 table header (requant.c
 
 @pytest.mark.parametrize("s_out", [0.36, 0.05])
 def test_requant_table4_threshold_neighbourhoods(s_out):
-    """The compact table gives up the low 8 bits of each threshold: drive y
+    """The compact table word keeps the threshold only to a 256-float run: drive y
     through +-600 ulps around every threshold word (acc = 0, so y = bias
     exactly) and through the non-folded (tiny scale) epilogue; every code
     must equal the oracle's direct evaluation."""
