@@ -53,9 +53,14 @@ constexpr int kBQ = 128, kBK = 128, kD = 64;
 constexpr int kStages = 3;
 constexpr int kQBytes = kBQ * kD * 2;      // 16 KB
 constexpr int kKVBytes = kBK * kD * 2;     // 16 KB
-constexpr int kThreads = 32 * 10;          // w0 TMA + TMEM alloc, w1 MMA, w2-5 softmax A, w6-9 softmax B
+// warpgroup 0: w0 TMA + TMEM alloc, w1 MMA, w2-3 idle; warpgroup 1: softmax A;
+// warpgroup 2: softmax B (setmaxnreg: 56 registers for warpgroup 0, 224 for the
+// softmax warpgroups, which keep a 128-score row in registers)
+constexpr int kThreads = 32 * 12;
+constexpr int kRegLaunch = 168, kRegCtl = 56, kRegSoft = 224;
+static_assert(kRegCtl * 128 + kRegSoft * 256 <= kRegLaunch * kThreads, "register split");
 constexpr float kRescale = 8.0f;
-constexpr int kSmem = 1024 + 4 * kQBytes + 2 * kStages * kKVBytes + 256;
+constexpr int kSmem = 1024 + 4 * kQBytes + 2 * kStages * kKVBytes + 512;
 
 #ifdef MKQ_TRACE
 // Diagnostics build only (tools/trace_attn.py): per-warp (tag, clock64)
@@ -112,7 +117,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* s_full = kv_empty + kStages;          // [2] per tile
     uint64_t* p_ready = s_full + 2;                 // [2] per tile
     uint64_t* o_done = p_ready + 2;                 // [2] per tile, once per item
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
+    uint64_t* s_free = o_done + 2;                  // [2] per tile: S_x(j) read into registers (j < nblk-1)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_free + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #ifdef MKQ_TRACE
@@ -132,6 +138,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_init(&p_ready[i], 4);
             ptx::mbar_init(&o_done[i], 1);
             ptx::mbar_init(&pv_done[i], 1);
+            ptx::mbar_init(&s_free[i], 4);
         }
         ptx::fence_barrier_init();
     }
@@ -147,6 +154,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto tO = [tmem](int x) { return tmem + (uint32_t)(2 * kBK + x * kD); };
     auto tP = [tmem](int x) { return tmem + (uint32_t)(2 * kBK + (2 + x) * kD); };
 
+    // setmaxnreg inside each role's branch (ptxas then allocates each region
+    // with its own budget)
+    if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegCtl));
     if (warp == 0) {
         // ---------------------------------------------------- TMA producer
         if (lane == 0) {
@@ -188,7 +199,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint64_t dK0 = ptx::desc_sw128_kmajor(ptx::smem_u32(sK));
         const uint64_t dV0 = desc_sw128_mnmajor(ptx::smem_u32(sV));
         int g = 0, it = 0, qb = 0;
-        uint32_t sph[2] = {0, 0};   // number of S issues per tile (p_ready parity source)
+        uint32_t sph[2] = {0, 0};   // number of P hand-overs per tile (p_ready parity source)
+        uint32_t fph[2] = {0, 0};   // number of S read-backs per tile (s_free parity source)
         Item I;
         auto issue_S = [&](int x, int gg) {
             const uint64_t dq = dQ0 + (uint64_t)((2 * qb + x) * (kQBytes >> 4));
@@ -221,12 +233,19 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int x = 0; x < 2; ++x) {
                     if (x == 1 && !I.hasB) break;
+                    // S_x(j+1) as soon as softmax x holds S_x(j) in registers, so it
+                    // computes under softmax x's exponentials (was: after P_x(j))
+                    if (more) {
+                        ptx::mbar_wait(&s_free[x], fph[x] & 1);
+                        ++fph[x];
+                        ptx::tc_fence_after();
+                        issue_S(x, g + 1);
+                    }
                     TRACE(10 + 10 * x);
                     ptx::mbar_wait(&p_ready[x], sph[x] & 1);
                     TRACE(11 + 10 * x);
                     ++sph[x];
                     ptx::tc_fence_after();
-                    if (more) issue_S(x, g + 1);
 #ifndef MKQ_ABL_NOPV
                     issue_PV(x, g, j);
 #endif
@@ -239,9 +258,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mma_commit_warp(&q_empty[qb]);
             ++it;
         }
+    }
     } else {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegSoft));
         // ---------------------------------------------------- softmax + epilogue
-        const int x = warp >= 6 ? 1 : 0;          // tile
+        const int x = warp >= 8 ? 1 : 0;          // tile
         const int q = warp & 3;                   // TMEM lane quadrant
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
         const float c = 0.125f * 1.4426950408889634f;   // 1/sqrt(64) * log2(e)
@@ -266,9 +287,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int cc = 0; cc < 4; ++cc)
                     for (int i = 0; i < 32; ++i) sv[cc][i] = __float_as_uint((float)((lane * 7 + i * 3 + cc) & 15));
 #else
-                for (int cc = 0; cc < 4; ++cc) ptx::tmem_ld_32x32b_x32(tS(x) + lane_off + 32 * cc, sv[cc]);
-                ptx::tmem_ld_wait();
+                // one 32-column load in flight per warp: tools/tmem_bench.cu measures
+                // 56 B/cycle/SM for ld.x32 + wait but 32 B/cycle/SM when a warp
+                // issues four x32 loads before waiting (profiles/r02_tmem_bench.md),
+                // and this readback is the kernel's bound
+                for (int cc = 0; cc < 4; ++cc) {
+                    ptx::tmem_ld_32x32b_x32(tS(x) + lane_off + 32 * cc, sv[cc]);
+                    ptx::tmem_ld_wait_regs(sv[cc]);
+                }
 #endif
+                if (j + 1 < I.nblk) {   // S_x's columns are free for S_x(j+1)
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(&s_free[x]);
+                }
                 const int kvalid = I.len - j * kBK;   // keys >= kvalid are masked (last block only)
                 if (kvalid < kBK) {
 #pragma unroll
@@ -306,12 +338,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     m = m_new;
                 }
-                // XU (exp2 + f32->f16 pack) turn-taking between the two tiles'
-                // warps of one quadrant (same SMSP): A(j) -> B(j) -> A(j+1)...
-                // so one tile's exponentials overlap the other's MMAs instead
-                // of both tiles contending for the XU pipe in lock-step.
+                // Optional (MKQ_ATTN_STAGGER, off): XU turn-taking between the two
+                // tiles' warps of one quadrant (same SMSP), A(j) -> B(j) -> A(j+1).
+                // Since S_x(j+1) is issued as soon as S_x(j) is read back, the
+                // turn-taking only delays the tiles (535 vs 482 us at C4).
                 TRACE(3);
-#ifndef MKQ_ABL_NOSTAGGER
+#ifdef MKQ_ATTN_STAGGER
                 if (I.hasB) {
                     if (x == 0 && j > 0) ptx::named_bar_sync(5 + q, 64);
                     if (x == 1) ptx::named_bar_sync(1 + q, 64);
@@ -347,7 +379,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
                     tmem_st_x16(tP(x) + lane_off + 16 * cc, pk);
                 }
-#ifndef MKQ_ABL_NOSTAGGER
+#ifdef MKQ_ATTN_STAGGER
                 if (I.hasB) {
                     if (x == 0) ptx::named_bar_arrive(1 + q, 64);
                     if (x == 1 && j + 1 < I.nblk) ptx::named_bar_arrive(5 + q, 64);
@@ -370,8 +402,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::tc_fence_after();
             uint32_t o[2][32];
             ptx::tmem_ld_32x32b_x32(tO(x) + lane_off, o[0]);
+            ptx::tmem_ld_wait_regs(o[0]);
             ptx::tmem_ld_32x32b_x32(tO(x) + lane_off + 32, o[1]);
-            ptx::tmem_ld_wait();
+            ptx::tmem_ld_wait_regs(o[1]);
             ptx::tc_fence_before();
             TRACE(8);
             if (row < I.len) {

@@ -68,7 +68,7 @@ struct Gemm2Cfg {
     // kLut4 register split (setmaxnreg; must fit the launch allocation)
     static constexpr int kRegLaunch = ((65536 / kThreads) & ~7) > 255 ? 248 : ((65536 / kThreads) & ~7);
     static constexpr int kRegProd = 40;
-    static constexpr int kRegUnp = kUnpWarps >= 8 ? 48 : 56;
+    static constexpr int kRegUnp = kUnpWarps >= 8 ? (kLut4 ? 40 : 48) : 56;
     static constexpr int kRegEpi =
         ((kRegLaunch * kThreads - 128 * kRegProd - 32 * kUnpWarps * kRegUnp) / (32 * kEpiWarps)) & ~7;
     static_assert(!kLut4 || (kRegEpi >= kRegLaunch && kRegEpi <= 256), "register split");

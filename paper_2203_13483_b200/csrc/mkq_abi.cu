@@ -468,6 +468,8 @@ mkq_status gemm_common(bool int4, const void* a, int64_t lda, const void* w, int
             if (many_epi && e.out == MKQ_OUT_I4 && p2.table && !no_lut4) {
                 if (lut4_epi == 8)
                     return launch_gemm2<mkq::Gemm2Cfg<256, 8, 4, true>>(a, lda, w, ldw, (int)M, (int)N, (int)K, p2, sms, st);
+                if (lut4_epi == 168)
+                    return launch_gemm2<mkq::Gemm2Cfg<256, 16, 8, true>>(a, lda, w, ldw, (int)M, (int)N, (int)K, p2, sms, st);
                 return launch_gemm2<mkq::Gemm2Cfg<256, 16, 4, true>>(a, lda, w, ldw, (int)M, (int)N, (int)K, p2, sms, st);
             }
             if (many_epi)

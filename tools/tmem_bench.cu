@@ -50,7 +50,12 @@ __device__ __forceinline__ void ld16x128_x16(uint32_t taddr, uint32_t (&r)[32]) 
         : "r"(taddr));
 }
 
-template <int MODE>   // 0: ld + wait each, 1: 4 lds then wait, 2: st x32 (+wait::st every 4), 3: 16x256b.x8, 4: 16x128b.x16
+// 0: ld + wait each (same columns every iteration), 1: 4 lds then wait (columns ^64/128/192),
+// 2: st x32 (+wait::st every 4), 3: 16x256b.x8, 4: 16x128b.x16,
+// 5: ld + wait, columns rotating over 8 x 32 (distinct data each time),
+// 6: 4 lds of consecutive 32-column chunks then wait (the attention S readback pattern),
+// 7: 2 lds (consecutive chunks) then wait
+template <int MODE>
 __global__ void k(int iters, uint32_t* out, long long* cyc) {
     __shared__ uint32_t slot;
     const int warp = threadIdx.x >> 5;
@@ -79,6 +84,26 @@ __global__ void k(int iters, uint32_t* out, long long* cyc) {
             ld32(base ^ 192, c);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             acc ^= r[it & 31] ^ a[(it + 1) & 31] ^ b[(it + 2) & 31] ^ c[(it + 3) & 31];
+        } else if (MODE == 5) {
+            ld32(base + 32u * (uint32_t)((it + (warp >> 2)) & 7), r);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            acc ^= r[it & 31];
+        } else if (MODE == 6) {
+            uint32_t a[32], b[32], c[32];
+            const uint32_t b0 = slot + ((uint32_t)((warp & 3) * 32) << 16) + 128u * (uint32_t)((it + (warp >> 2)) & 3);
+            ld32(b0, r);
+            ld32(b0 + 32, a);
+            ld32(b0 + 64, b);
+            ld32(b0 + 96, c);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            acc ^= r[it & 31] ^ a[(it + 1) & 31] ^ b[(it + 2) & 31] ^ c[(it + 3) & 31];
+        } else if (MODE == 7) {
+            uint32_t a[32];
+            const uint32_t b0 = slot + ((uint32_t)((warp & 3) * 32) << 16) + 64u * (uint32_t)((it + (warp >> 2)) & 7);
+            ld32(b0, r);
+            ld32(b0 + 32, a);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            acc ^= r[it & 31] ^ a[(it + 1) & 31];
         } else if (MODE == 3) {
             ld16x256_x8(base, r);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
@@ -107,18 +132,21 @@ int main() {
     long long* c;
     cudaMalloc(&o, 1 << 24);
     cudaMalloc(&c, 8);
-    const char* nm[] = {"ld.x32 + wait", "4 x ld.x32 + wait", "st.x32", "16x256b.x8 + wait", "16x128b.x16 + wait"};
+    const char* nm[] = {"ld.x32 + wait", "4 x ld.x32 + wait", "st.x32", "16x256b.x8 + wait", "16x128b.x16 + wait",
+                        "ld.x32 rotating", "4 x ld.x32 consec", "2 x ld.x32 consec"};
+    void (*fs[])(int, uint32_t*, long long*) = {k<0>, k<1>, k<2>, k<3>, k<4>, k<5>, k<6>, k<7>};
+    const int mult[] = {1, 4, 1, 1, 1, 1, 4, 2};
     for (int warps : {4, 8, 16}) {
-        for (int m = 0; m < 5; ++m) {
+        for (int m = 0; m < 8; ++m) {
             const int iters = 4000;
-            void (*f)(int, uint32_t*, long long*) = m == 0 ? k<0> : (m == 1 ? k<1> : (m == 2 ? k<2> : (m == 3 ? k<3> : k<4>)));
+            void (*f)(int, uint32_t*, long long*) = fs[m];
             f<<<148, 32 * warps>>>(iters, o, c);
             long long h;
             cudaError_t e = cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
             if (e != cudaSuccess) { printf("err %s\n", cudaGetErrorString(e)); return 1; }
-            const double bytes = (double)iters * warps * 4096 * (m == 1 ? 4 : 1);
+            const double bytes = (double)iters * warps * 4096 * mult[m];
             printf("warps=%2d %-18s %7.1f B/cycle/SM (%.0f cycles per op per warp)\n", warps, nm[m], bytes / h,
-                   (double)h / iters / (m == 1 ? 4 : 1));
+                   (double)h / iters / mult[m]);
         }
     }
     return 0;

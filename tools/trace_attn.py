@@ -13,7 +13,8 @@ from paper_2203_13483_b200 import build as B
 dbg = os.path.join(ROOT, "build_dbg", "libmkq.so")
 if not os.environ.get("NO_BUILD"):
     os.makedirs(os.path.dirname(dbg), exist_ok=True)
-    subprocess.check_call([B.NVCC, *B.FLAGS, "-DMKQ_TRACE", "-o", dbg, os.path.join(B.CSRC, "mkq_abi.cu"), "-ldl"])
+    extra = os.environ.get("EXTRA_FLAGS", "").split()
+    subprocess.check_call([B.NVCC, *B.FLAGS, "-DMKQ_TRACE", *extra, "-o", dbg, os.path.join(B.CSRC, "mkq_abi.cu"), "-ldl"])
 os.environ["MKQ_LIB"] = dbg
 import torch
 from paper_2203_13483_b200 import mkq as M
@@ -25,21 +26,22 @@ qkv = (torch.randn(T, 3 * hd, device="cuda") * 0.8).half()
 out = torch.empty(T, hd // 2, dtype=torch.uint8, device="cuda")
 M.mkq_attention(qkv, H, Bn, S, None, mode=M.OUT_I4, s_out=0.05, out=out)
 slots = 512
-buf = torch.zeros(10 * slots * 2, dtype=torch.int64, device="cuda")
+NW = 12   # warps per CTA (attention_pp_sm100.cuh kThreads / 32)
+buf = torch.zeros(NW * slots * 2, dtype=torch.int64, device="cuda")
 assert lib().mkq_debug_set_trace(ctypes.c_void_p(buf.data_ptr())) == 0
 torch.cuda.synchronize()
 M.mkq_attention(qkv, H, Bn, S, None, mode=M.OUT_I4, s_out=0.05, out=out)
 torch.cuda.synchronize()
-tr = buf.view(10, slots, 2).cpu().numpy()
-t0 = min(int(tr[w, 0, 1]) for w in range(10) if tr[w, 0, 1])
+tr = buf.view(NW, slots, 2).cpu().numpy()
+t0 = min(int(tr[w, 0, 1]) for w in range(NW) if tr[w, 0, 1])
 nshow = int(os.environ.get("N", 60))
-for w in [int(x) for x in os.environ.get("WARPS", "1,2,6").split(",")]:
+for w in [int(x) for x in os.environ.get("WARPS", "1,4,8").split(",")]:
     ev = [(int(a), int(b) - t0) for a, b in tr[w] if b]
     print(f"warp {w}: {len(ev)} events")
     print("  " + " ".join(f"{a}@{b}" for a, b in ev[:nshow]))
 # summary: per-softmax-warp time split
 import collections
-for w in range(2, 10):
+for w in range(4, NW):
     ev = [(int(a), int(b)) for a, b in tr[w] if b]
     acc = collections.Counter()
     for (a, ta), (b, tb) in zip(ev, ev[1:]):
