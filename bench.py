@@ -669,28 +669,19 @@ def c3_encoder(torch, dev, reps=20):
             L = model.build_layer(p, bits, dev)
             model.calibrate(L, torch.from_numpy(synth.hidden_states(4, S, h, seed=1000000 + i)).to(dev), 4, S)
             layers.append(L)
-        enc = model.Encoder(layers)
         out = torch.empty_like(hin)
-        st = torch.cuda.Stream(device=dev)
-        with torch.cuda.stream(st):
-            for _ in range(2):
-                enc(hin, B, S, out=out, stream=st)
-            torch.cuda.synchronize(dev)
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=st):
-                enc(hin, B, S, out=out, stream=st)
-            g.replay()
-            torch.cuda.synchronize(dev)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(st)
-            for _ in range(reps):
-                g.replay()
-            e1.record(st)
-            torch.cuda.synchronize(dev)
-        ms = e0.elapsed_time(e1) / reps
-        res[name] = {"plan": "".join(str(b) for b in plan), "ms": round(ms, 4),
-                     "tops": round(12 * linear_ops(T, h, F) / (ms * 1e-3) / 1e12, 1),
-                     "compression_vs_fp32": round(model.compression_ratio(plan), 3)}
+        # fused glue (LN2 writes the next layer's codes, NEXT(4)) and, for the
+        # paper's mixed plan, the unfused stack for comparison
+        for fuse in ((True, False) if name.startswith("mixed") else (True,)):
+            enc = model.Encoder(layers, fuse_codes=fuse)
+            ms = graph_time(torch, lambda st: enc(hin, B, S, out=out, stream=st), dev, reps=reps)
+            if fuse:
+                res[name] = {"plan": "".join(str(b) for b in plan), "ms": round(ms, 4),
+                             "tops": round(12 * linear_ops(T, h, F) / (ms * 1e-3) / 1e12, 1),
+                             "compression_vs_fp32": round(model.compression_ratio(plan), 3),
+                             "fused_layer_codes": True}
+            else:
+                res[name]["unfused_ms"] = round(ms, 4)
     return res
 
 

@@ -295,6 +295,20 @@ typedef struct {
      * mkq_attention_i8 (max_seq <= 128); 0 = fp16 q|k|v (R10). */
     int32_t int_attention;
     float s_attn;
+    /* NEXT(4) fused glue across a layer stack (optional; NULL / 0 = off):
+     * in_codes  [device] the Eq.1 codes of h_in with (s_qkv_in, bits), packed as
+     *           mkq_quantize_pack writes them ([tokens, hidden*bits/8], row
+     *           stride hidden*bits/8 bytes, 16-byte aligned): the input
+     *           quantize (a1) is skipped -- the previous layer's LN2 wrote them;
+     * out_codes [device] LN2 also writes the Eq.1 codes of h_out with
+     *           (s_out_codes, out_bits in {4, 8}; codes [-8,7] / [-128,127])
+     *           in that layout: the next layer's in_codes.  Bit-identical to
+     *           quantizing h_out separately (the LN kernel's fused quantize).
+     * in_codes may equal out_codes (the QKV GEMM reads it before LN2 writes). */
+    const void *in_codes;
+    void *out_codes;
+    float s_out_codes;
+    int32_t out_bits;
 } mkq_layer;
 
 /* Workspace bytes for `tokens` rows (intermediates of one layer). */

@@ -57,7 +57,9 @@ class MkqLayer(ctypes.Structure):
         [(n, ctypes.c_void_p) for n in ("w_qkv", "w_o", "w_1", "w_2", "sw_qkv", "sw_o", "sw_1", "sw_2",
                                         "b_qkv", "b_o", "b_1", "b_2", "ln1_g", "ln1_b", "ln2_g", "ln2_b")] + \
         [(n, ctypes.c_float) for n in ("s_qkv_in", "s_o_in", "s_ffn1_in", "s_ffn2_in", "ln_eps")] + \
-        [("ffn1_requant_table", ctypes.c_void_p), ("int_attention", ctypes.c_int32), ("s_attn", ctypes.c_float)]
+        [("ffn1_requant_table", ctypes.c_void_p), ("int_attention", ctypes.c_int32), ("s_attn", ctypes.c_float),
+         ("in_codes", ctypes.c_void_p), ("out_codes", ctypes.c_void_p), ("s_out_codes", ctypes.c_float),
+         ("out_bits", ctypes.c_int32)]
 
 
 class MkqError(RuntimeError):

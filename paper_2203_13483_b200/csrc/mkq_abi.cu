@@ -1043,6 +1043,12 @@ mkq_status mkq_bert_layer(const mkq_layer* L, const float* h_in, int64_t batch, 
     if (L->int_attention != 0 && L->int_attention != 1) return fail(MKQ_ERR_RANGE, "int_attention must be 0 or 1");
     if (L->int_attention && !finite_pos(L->s_attn)) return fail(MKQ_ERR_SCALE, "s_attn must be > 0 and finite");
     if (L->int_attention && max_seq > 128) return fail(MKQ_ERR_SHAPE, "int_attention needs max_seq <= 128");
+    if (L->in_codes && !aligned16(L->in_codes)) return fail(MKQ_ERR_ALIGN, "in_codes must be 16-byte aligned");
+    if (L->out_codes) {
+        if (L->out_bits != 4 && L->out_bits != 8) return fail(MKQ_ERR_RANGE, "out_bits must be 4 or 8");
+        if (!finite_pos(L->s_out_codes)) return fail(MKQ_ERR_SCALE, "s_out_codes must be > 0 and finite");
+        if (!aligned16(L->out_codes)) return fail(MKQ_ERR_ALIGN, "out_codes must be 16-byte aligned");
+    }
     const LayerWs W = layer_ws(L, T);
     if (ws_bytes < W.total) return fail(MKQ_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes, W.total);
     if (!aligned16(ws)) return fail(MKQ_ERR_ALIGN, "workspace must be 16-byte aligned");
@@ -1073,8 +1079,12 @@ mkq_status mkq_bert_layer(const mkq_layer* L, const float* h_in, int64_t batch, 
         mkq_status _s = (x);             \
         if (_s != MKQ_OK) return _s;     \
     } while (0)
-    // a1: quantize the layer input (per-tensor static scale, by value)
-    MKQ_TRY(quantize_internal(h_in, T, h, h, nullptr, L->s_qkv_in, 0, bits, qlo, qhi, codes_in, cbh, sms, st));
+    // a1: quantize the layer input (per-tensor static scale, by value), unless
+    // the previous layer's LN2 already wrote these codes (in_codes)
+    if (L->in_codes)
+        codes_in = static_cast<uint8_t*>(const_cast<void*>(L->in_codes));
+    else
+        MKQ_TRY(quantize_internal(h_in, T, h, h, nullptr, L->s_qkv_in, 0, bits, qlo, qhi, codes_in, cbh, sms, st));
     // a2-a4: QKV projection -> fp16 q|k|v (R10)
     if (L->int_attention) {
         // NEXT(2): int8 q|k|v codes (Eq.1, s_attn, [-127,127]) -> integer attention core (R19)
@@ -1105,9 +1115,11 @@ mkq_status mkq_bert_layer(const mkq_layer* L, const float* h_in, int64_t batch, 
     // FFN2 -> fp32
     MKQ_TRY(gemm(codes_ffn2, cbf, L->w_2, cbf, T, h, F, L->s_ffn2_in, L->sw_2, L->b_2, &e_f32, f, h * 4, nullptr,
                  0, stream));
-    // LN2(f + h1) -> h_out
-    MKQ_TRY(mkq_residual_layernorm(f, h1, T, h, h, L->ln2_g, L->ln2_b, L->ln_eps, h_out, 0, 1.0f, 0, 0, nullptr,
-                                   0, stream));
+    // LN2(f + h1) -> h_out (+ the next layer's input codes, fused a1)
+    const int ob = L->out_codes ? L->out_bits : 0;
+    MKQ_TRY(mkq_residual_layernorm(f, h1, T, h, h, L->ln2_g, L->ln2_b, L->ln_eps, h_out, ob,
+                                   ob ? L->s_out_codes : 1.0f, ob == 4 ? -8 : -128, ob == 4 ? 7 : 127, L->out_codes,
+                                   ob == 4 ? h / 2 : h, stream));
 #undef MKQ_TRY
     return MKQ_OK;
 }

@@ -289,15 +289,27 @@ class QLayer:
 
 def mkq_bert_layer(layer: QLayer, h_in: torch.Tensor, batch: int, max_seq: int,
                    cu_seqlens: Optional[torch.Tensor] = None, h_out: Optional[torch.Tensor] = None,
-                   ws: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
-    """One quantized post-LN BERT layer on h_in fp32 [tokens, hidden]."""
+                   ws: Optional[torch.Tensor] = None, stream=None, in_codes: Optional[torch.Tensor] = None,
+                   out_codes: Optional[torch.Tensor] = None, s_out_codes: float = 0.0,
+                   out_bits: int = 0) -> torch.Tensor:
+    """One quantized post-LN BERT layer on h_in fp32 [tokens, hidden].
+    in_codes: h_in's Eq.1 codes (s_qkv_in, layer.bits), written by the previous
+    layer's LN2 (skips the input quantize); out_codes: LN2 also writes h_out's
+    codes with (s_out_codes, out_bits) for the next layer (mkq_layer fields)."""
     T = h_in.shape[0]
     if h_out is None:
         h_out = torch.empty_like(h_in)
     need = layer.workspace_size(T)
     if ws is None or ws.numel() < need:
         ws = torch.empty(need, dtype=torch.uint8, device=h_in.device)
+    c = layer.c
+    if in_codes is not None or out_codes is not None:
+        c = MkqLayer.from_buffer_copy(layer.c)
+        c.in_codes = _ptr(in_codes)
+        c.out_codes = _ptr(out_codes)
+        c.s_out_codes = float(s_out_codes)
+        c.out_bits = int(out_bits)
     check("mkq_bert_layer", lib().mkq_bert_layer(
-        ctypes.byref(layer.c), _ptr(h_in), batch, max_seq, _ptr(cu_seqlens), T, _ptr(h_out), _ptr(ws), ws.numel(),
+        ctypes.byref(c), _ptr(h_in), batch, max_seq, _ptr(cu_seqlens), T, _ptr(h_out), _ptr(ws), ws.numel(),
         _stream(stream)))
     return h_out

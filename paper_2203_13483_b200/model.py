@@ -107,12 +107,18 @@ def compression_ratio(plan: Sequence[int]) -> float:
 
 class Encoder:
     """A stack of quantized BERT layers run back to back through
-    mkq_bert_layer on one stream (CUDA-graph capturable)."""
+    mkq_bert_layer on one stream (CUDA-graph capturable).
 
-    def __init__(self, layers: List[M.QLayer]):
+    fuse_codes (NEXT(4) fused glue, default on): layer i's LN2 also writes
+    layer i+1's input codes (Eq.1 with layer i+1's s_qkv_in and bits), so every
+    layer after the first skips its input quantize pass; bit-identical to the
+    unfused stack (tests/test_gpu_layer.py)."""
+
+    def __init__(self, layers: List[M.QLayer], fuse_codes: bool = True):
         self.layers = layers
+        self.fuse_codes = fuse_codes
         self._ws = None
-        self._buf = None
+        self._codes = None
 
     def __call__(self, h: torch.Tensor, batch: int, max_seq: int, cu_seqlens=None, stream=None,
                  out: Optional[torch.Tensor] = None) -> torch.Tensor:
@@ -121,9 +127,20 @@ class Encoder:
         need = max(l.workspace_size(T) for l in self.layers)
         if self._ws is None or self._ws.numel() < need or self._ws.device != h.device:
             self._ws = torch.empty(need, dtype=torch.uint8, device=h.device)
+        cb = max(l.hidden * l.bits // 8 for l in self.layers)
+        if self.fuse_codes and (self._codes is None or self._codes.numel() < T * cb or self._codes.device != h.device):
+            self._codes = torch.empty(T * cb, dtype=torch.uint8, device=h.device)
         cur = h
-        for l in self.layers:
-            cur = M.mkq_bert_layer(l, cur, batch, max_seq, cu_seqlens, h_out=out, ws=self._ws, stream=stream)
+        n = len(self.layers)
+        for i, l in enumerate(self.layers):
+            kw = {}
+            if self.fuse_codes:
+                if i > 0:
+                    kw["in_codes"] = self._codes
+                if i + 1 < n:
+                    nxt = self.layers[i + 1]
+                    kw.update(out_codes=self._codes, s_out_codes=nxt.scales["s_qkv_in"], out_bits=nxt.bits)
+            cur = M.mkq_bert_layer(l, cur, batch, max_seq, cu_seqlens, h_out=out, ws=self._ws, stream=stream, **kw)
             if out is None:
                 out = cur
         return cur

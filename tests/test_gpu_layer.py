@@ -184,6 +184,21 @@ def test_mixed_precision_encoder_runs():
     out = host(enc(h, 2, 32, out=torch.empty_like(h)))
     assert np.isfinite(out).all()
     assert np.allclose(out.mean(-1), 0.0, atol=0.1)
+    # NEXT(4) fused glue: LN2 writing the next layer's codes (incl. the 8 -> 4
+    # bit switch between layers 2 and 3) is bit-identical to the unfused stack
+    ref = host(model.Encoder(layers, fuse_codes=False)(h, 2, 32, out=torch.empty_like(h)))
+    assert np.array_equal(out, ref)
+    # and each layer's input codes equal mkq_quantize_pack of its input
+    cur = h.clone()
+    for i, L in enumerate(layers[:-1]):
+        nxt = layers[i + 1]
+        codes = torch.empty(64 * 128 * 8 // 8, dtype=torch.uint8, device=DEV)
+        cur = M.mkq_bert_layer(L, cur, 2, 32, out_codes=codes, s_out_codes=nxt.scales["s_qkv_in"],
+                               out_bits=nxt.bits)
+        lo, hi = model.act_range(nxt.bits)
+        ref_c = M.mkq_quantize_pack(cur, torch.tensor([nxt.scales["s_qkv_in"]], device=DEV), nxt.bits, lo, hi)
+        n = ref_c.numel() * ref_c.element_size()
+        assert torch.equal(codes[:n], ref_c.contiguous().view(torch.uint8).reshape(-1))
 
 
 def _oracle_weights(p, bits, scales):
