@@ -166,6 +166,28 @@ MKQ_API mkq_status mkq_gemm_w8a8(const void *a, int64_t lda_bytes, const void *w
  * sums the exact int32 partials (R15) through distributed shared memory. */
 MKQ_API size_t mkq_gemm_workspace_size(int64_t M, int64_t N, int64_t K);
 
+/* NEXT(4) fused glue (the residual + post-LN of P:79-100 / R9
+ * fused into the W4A4 GEMM that produces its input):
+ *   y = LN(fma((float)acc, fl(s_a*s_w[n]), b[n]) + res; gamma, beta, eps)
+ *   [+ q = Eq.1 codes of y with (s_q, q_bits, qmin, qmax)]
+ * acc as mkq_gemm_w4a4 (a [M, K] packed int4 codes, w [N, K] packed int4);
+ * res, y [device] fp32 [M, N] (row strides ldr / ldy elements, 16-byte
+ * aligned rows); gamma, beta [device] fp32 [N]; q [device] packed codes
+ * [M, N*q_bits/8] (row stride ldq bytes, 16-byte aligned; q_bits 0 = none).
+ * N = 256 * np, np in [1, 4] (hidden 256..1024), K % 32 == 0.  LN statistics
+ * are the two-pass mean / centred variance of residual_ln (fp32, different
+ * summation order: results agree with mkq_gemm_w4a4 + mkq_residual_layernorm
+ * within LN rounding, and are deterministic).  ws >=
+ * mkq_gemm_residual_ln_workspace_size(M, N) bytes (row-statistics exchange
+ * between the CTAs of a row; the call zeroes its counters on `stream`). */
+MKQ_API size_t mkq_gemm_residual_ln_workspace_size(int64_t M, int64_t N);
+MKQ_API mkq_status mkq_gemm_residual_ln(const void *a, int64_t lda_bytes, const void *w, int64_t ldw_bytes,
+                                        int64_t M, int64_t N, int64_t K, float s_a, const float *s_w,
+                                        const float *bias, const float *res, int64_t ldr, const float *gamma,
+                                        const float *beta, float eps, float *y, int64_t ldy, int q_bits,
+                                        float s_q, int qmin, int qmax, void *q, int64_t ldq, void *ws,
+                                        size_t ws_bytes, void *stream);
+
 /* Diagnostics / tests: GEMM tile plan for small M.  -1 = heuristic (default;
  * also the MKQ_SMALL_M environment variable), 0 = never the small-M plan,
  * 1 = always the tcgen05 cluster split-K plan, 2 = always the mma.sync

@@ -30,6 +30,9 @@ SIGNATURES = {
     "mkq_gemm_w4a4": (I32, [P, I64, P, I64, I64, I64, I64, F32, P, P, P, P, I64, P, SZ, P]),
     "mkq_gemm_w8a8": (I32, [P, I64, P, I64, I64, I64, I64, F32, P, P, P, P, I64, P, SZ, P]),
     "mkq_gemm_workspace_size": (SZ, [I64, I64, I64]),
+    "mkq_gemm_residual_ln_workspace_size": (SZ, [I64, I64]),
+    "mkq_gemm_residual_ln": (I32, [P, I64, P, I64, I64, I64, I64, F32, P, P, P, I64, P, P, F32, P, I64, I32, F32,
+                                   I32, I32, P, I64, P, SZ, P]),
     "mkq_set_small_m_mode": (None, [I32]),
     "mkq_requant_table_size": (SZ, []),
     "mkq_requant_table": (I32, [I32, F32, I32, I32, P, SZ, P]),

@@ -31,13 +31,38 @@
 
 namespace mkq {
 
+// Fused residual + LayerNorm (+ Eq.1 quantize) epilogue (kLn, NEXT(4) fused
+// glue): y = LN(dequant(acc) + res) over full rows of N = 256 np columns.
+// The np CTA pairs of a "group" compute the np 256-column tiles of the same
+// 256 rows at the same time and exchange per-row partial sums (mean, then the
+// centred sum of squares) through global memory (workspace `stats`, arrival
+// counters `flags`, zeroed by the launcher before every launch).
+struct Ln2Params {
+    const float* res;                 // residual [M, N] fp32, row stride ldr elements
+    int64_t ldr;
+    const float *g, *b;               // LN gamma / beta [N]
+    float eps;
+    float* y;                         // LN output [M, N] fp32, row stride ldy elements
+    int64_t ldy;
+    uint8_t* q;                       // optional Eq.1 codes of y (qbits 4|8; 0 = none)
+    int64_t ldq;
+    int qbits, qmin, qmax;
+    float s_q;
+    float* stats;                     // [groups][2 buffers][2 stages][np][256 rows]
+    uint32_t* flags;                  // [groups][2][2] counters, 32-byte stride
+    int np;                           // 256-column tiles per row = CTA pairs per group
+};
+
 struct Epi2Params {
     EpiParams e;
     const void* table;   // rq table (global) or null
+    Ln2Params ln;        // kLn only
 };
 
-template <int BN_, int EPI_ = 8, int UNP_ = 8, bool LUT4_ = false>
+template <int BN_, int EPI_ = 8, int UNP_ = 8, bool LUT4_ = false, bool LN_ = false>
 struct Gemm2Cfg {
+    static constexpr bool kLn = LN_;                 // fused residual + LayerNorm epilogue
+    static constexpr bool kRegSplit = LUT4_ || LN_;  // setmaxnreg per role
     static constexpr bool kLut4 = LUT4_;             // int4 output through the compact requant table
     static constexpr int BM = 128;                  // A rows per CTA (MMA M = 256 per pair)
     static constexpr int BN = BN_;                  // MMA N (per pair)
@@ -49,31 +74,37 @@ struct Gemm2Cfg {
     static constexpr int kAP = BM * BK / 2;
     static constexpr int kBP = BNH * BK / 2;
     static constexpr int kStageP = kAP + kBP;
-    static constexpr int S8 = 4;
-    static constexpr int SP = 3;
+    static constexpr int S8 = LN_ ? 3 : 4;            // kLn: smem goes to the epilogue's TMA staging
+    static constexpr int SP = LN_ ? 2 : 3;
     static constexpr int kEpiWarps = EPI_;          // 8 or 16 (2 or 4 per TMEM lane quadrant)
     static constexpr int kUnpWarps = UNP_;          // 8 or 4
     static constexpr int kThreads = 32 * (4 + kEpiWarps + kUnpWarps);
     static constexpr uint32_t kTmemCols = 2 * BN;
     static constexpr int kColsPerWarp = BN / (kEpiWarps / 4);
     // (sc, b) per column: 2 tile buffers x BN (shared by the epilogue), or
-    // (kLut4) one private kColsPerWarp slice per epilogue warp
-    static constexpr int kScb = kLut4 ? kEpiWarps * kColsPerWarp * 8 : 2 * BN * 8;
+    // (kLut4) one private kColsPerWarp slice per epilogue warp, or (kLn)
+    // (sc, b, gamma, beta) of the BN fixed columns + the quadrant partial sums
+    static constexpr int kScb = kLn ? BN * 16 + (kEpiWarps / 4) * BM * 8
+                                    : (kLut4 ? kEpiWarps * kColsPerWarp * 8 : 2 * BN * 8);
     // per epilogue warp: kLut4 one or (8 warps) two 32 x 16 B int4 blocks
-    // (double-buffered TMA stores), else one 32 x 64 B output block
+    // (double-buffered TMA stores), else one 32 x 64 B output block; kLn
+    // stores from registers
     static constexpr int kStgBufs = kLut4 && EPI_ <= 8 ? 2 : 1;
-    static constexpr int kStagePerWarp = kLut4 ? 512 * kStgBufs : 2048;
+    // kLn: two 32 x 32 fp32 SWIZZLE_128B blocks (residual in / LN output out)
+    // and two 32-row code blocks (<= 32 B per row) per warp
+    static constexpr int kStagePerWarp = kLn ? 2 * 4096 + 2 * 1024 : (kLut4 ? 512 * kStgBufs : 2048);
     static constexpr int kStaging = kEpiWarps * kStagePerWarp;
-    static constexpr int kTabBytes = kLut4 ? (int)rq::kSmem4Bytes : (int)rq::kSmemBytes;
+    static constexpr int kTabBytes = kLn ? 0 : (kLut4 ? (int)rq::kSmem4Bytes : (int)rq::kSmemBytes);
     // kLut4 register split (setmaxnreg; must fit the launch allocation)
     static constexpr int kRegLaunch = ((65536 / kThreads) & ~7) > 255 ? 248 : ((65536 / kThreads) & ~7);
     static constexpr int kRegProd = 40;
     static constexpr int kRegUnp = kUnpWarps >= 8 ? (kLut4 ? 40 : 48) : 56;
     static constexpr int kRegEpi =
         ((kRegLaunch * kThreads - 128 * kRegProd - 32 * kUnpWarps * kRegUnp) / (32 * kEpiWarps)) & ~7;
-    static_assert(!kLut4 || (kRegEpi >= kRegLaunch && kRegEpi <= 256), "register split");
+    static_assert(!kRegSplit || (kRegEpi >= kRegLaunch && kRegEpi <= 256), "register split");
+    static_assert(!kLn || (BN == 256 && !kLut4), "kLn: 256-column tiles");
     static_assert(kColsPerWarp % 32 == 0, "epilogue column split");
-    static constexpr int kBarBytes = 8 * (2 * S8 + 2 * SP + 4) + 16;
+    static constexpr int kBarBytes = 8 * (2 * S8 + 2 * SP + 4 + (LN_ ? 2 * EPI_ : 0)) + 16;
     static constexpr int kSmem = 1024 + S8 * kStage8 + SP * kStageP + kTabBytes + kScb + kStaging + kBarBytes;
     static_assert(kSmem <= 232448, "shared memory budget");
     static_assert(BN == 256 || BN == 128, "BN");
@@ -278,6 +309,44 @@ __device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {   // two 
     return *reinterpret_cast<float2*>(&r);
 }
 
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {   // two IEEE RN adds, one instruction
+    uint64_t r;
+    asm("add.rn.f32x2 %0, %1, %2;"
+        : "=l"(r)
+        : "l"(*reinterpret_cast<const uint64_t*>(&a)), "l"(*reinterpret_cast<const uint64_t*>(&b)));
+    return *reinterpret_cast<float2*>(&r);
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {   // two IEEE RN multiplies, one instruction
+    uint64_t r;
+    asm("mul.rn.f32x2 %0, %1, %2;"
+        : "=l"(r)
+        : "l"(*reinterpret_cast<const uint64_t*>(&a)), "l"(*reinterpret_cast<const uint64_t*>(&b)));
+    return *reinterpret_cast<float2*>(&r);
+}
+
+// Eq.1 codes of 8 values with one scale, int4 nibbles packed (value i in
+// nibble i), for epilogues where |code| is small: q = fl(x * RN(1/s)) differs
+// from fl(x / s) by at most 2 ulps of |q| <= 2^-19 inside the code range
+// [qmin, qmax] (|q| <= 8 after the clamp), so rint(clamp(q)) equals Eq.1's
+// rint(clamp(fl(x/s))) unless q lies within 2^-18 of a half-integer, which the
+// caller's `near` reports (evaluate those groups with quant_code).  Clamping
+// before rounding is rounding before clamping for integer bounds.
+__device__ __forceinline__ uint32_t quant_nib8_fast(const float (&x)[8], const QuantRcp& Q, bool& near) {
+    uint32_t w = 0;
+#pragma unroll
+    for (int i = 0; i < 8; i += 2) {
+        float2 q = mul2(make_float2(x[i], x[i + 1]), make_float2(Q.r, Q.r));
+        q.x = fminf(fmaxf(q.x, Q.lo), Q.hi);
+        q.y = fminf(fmaxf(q.y, Q.lo), Q.hi);
+        const float2 t = add2(q, make_float2(12582912.0f, 12582912.0f));
+        const float2 d = fma2(add2(t, make_float2(-12582912.0f, -12582912.0f)), make_float2(-1.0f, -1.0f), q);
+        near |= fabsf(fabsf(d.x) - 0.5f) <= 0x1p-18f;
+        near |= fabsf(fabsf(d.y) - 0.5f) <= 0x1p-18f;
+        w |= ((__float_as_uint(t.x) & 0xFu) << (4 * i)) | ((__float_as_uint(t.y) & 0xFu) << (4 * i + 4));
+    }
+    return w;
+}
+
 // A register the compiler cannot prove warp-uniform or constant: keeps values
 // used by every output in one vector register (a uniform value feeding an FFMA
 // that already takes a uniform operand is otherwise re-copied per use, and a
@@ -380,10 +449,297 @@ __device__ __forceinline__ void epi_lut4(const EpiParams& ep, const uint32_t (&v
     }
 }
 
+__device__ __forceinline__ void st_relaxed_gpu_u64(uint64_t* p, uint64_t v) {
+    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_relaxed_gpu_u64(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Acquire load of a global arrival counter (polled by one lane).
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Tensor maps of the kLn epilogue: residual and LN output fp32 [M, N] in
+// 32 x 32 SWIZZLE_128B boxes, the codes [M, N*qbits/8] in 32-row boxes of
+// 16 (int4) or 32 (int8) bytes.
+struct LnMaps {
+    CUtensorMap r, y, q;
+};
+
+// kLn epilogue (Ln2Params): per tile, thread = one row of this CTA's 128, warp
+// = one TMEM lane quadrant x kColsPerWarp columns.  The row's residual comes
+// in by TMA (32 x 32 fp32 SWIZZLE_128B boxes, two per warp in flight; lane l
+// reads its row's 16-byte chunks conflict-free), the accumulator is read once
+// (dequant exactly as the plain epilogue: fma((float)acc, fl(s_a s_w[n])
+// [2^-8 folded], b[n])), r = y + res (R9) is kept in registers and the TMEM
+// buffer released.  Row statistics: each warp's (mean, M2 = sum (r - mean)^2)
+// of its columns, combined over the warps of the quadrant and then over the
+// np column tiles of the row group (Chan et al.'s pairwise update, fixed
+// order: identical results in every CTA) through the group's `stats` slot,
+// one arrival per (CTA, quadrant) on the slot's counter.  Output: y = (r -
+// mean) * rstd * gamma + beta with rstd = rsqrt(M2 / N + eps) (the centred
+// two-pass statistics of residual_ln), staged in the same swizzled boxes and
+// TMA-stored, and optionally its Eq.1 codes.
+template <class Cfg>
+__device__ __forceinline__ void ln_epilogue(const Epi2Params& p, const LnMaps& lm, uint32_t tmem_base, uint64_t* tfull,
+                                            uint64_t* tempty, uint64_t* rbars, uint8_t* staging, float* colp_raw,
+                                            int t_begin, int t_step, int t_end, int group, int j, int M, int N,
+                                            int rank) {
+    constexpr int BM = Cfg::BM, BN = Cfg::BN, kCW = Cfg::kColsPerWarp, kQW = Cfg::kEpiWarps / 4;
+    constexpr int kCh = kCW / 32;
+    constexpr int kEpiThreads = 32 * Cfg::kEpiWarps;
+    static_assert(kCh % 2 == 0, "chunk pairs");
+    const EpiParams& ep = p.e;
+    const Ln2Params& L = p.ln;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int e = warp - 4, q = warp & 3, hsl = e >> 2;   // quadrant, column slice
+    const int et = threadIdx.x - 128;
+    const int np = L.np;
+    const int ncol0 = j * BN;                              // this pair's columns [ncol0, +BN)
+    // column parameters (fixed for the whole kernel) per column pair c2:
+    // dq[c2] = (sc, sc', b, b') (dequant, f32x2), ln[c2] = (g, g', beta, beta')
+    float4* dq = reinterpret_cast<float4*>(colp_raw);
+    float4* lnp = dq + BN / 2;
+    float2* qpart = reinterpret_cast<float2*>(colp_raw + 4 * BN);   // [kQW][BM] (mean, M2) per warp slice
+    float* dqf = reinterpret_cast<float*>(dq);
+    float* lnf = reinterpret_cast<float*>(lnp);
+    bool tiny = false;
+    for (int c = et; c < BN; c += kEpiThreads) {
+        const int n = ncol0 + c, o4 = 4 * (c >> 1) + (c & 1);
+        const float sc = __fmul_rn(ep.s_a, __ldg(ep.s_w + n));
+        tiny = tiny || !(sc >= 0x1p-118f);
+        dqf[o4] = sc;
+        dqf[o4 + 2] = ep.bias ? __ldg(ep.bias + n) : 0.0f;
+        lnf[o4] = __ldg(L.g + n);
+        lnf[o4 + 2] = __ldg(L.b + n);
+    }
+    const bool fold = !ptx::named_bar_sync_or(1, kEpiThreads, tiny);
+    if (fold)
+        for (int c = et; c < BN; c += kEpiThreads) {
+            const int o4 = 4 * (c >> 1) + (c & 1);
+            dqf[o4] = __fmul_rn(dqf[o4], 0x1p-8f);
+        }
+    ptx::named_bar_sync(1, kEpiThreads);
+    const QuantRcp Qr = quant_rcp(L.s_q, L.qmin, L.qmax);
+    const int row_l = q * 32 + lane;                       // row within the CTA's 128
+    const int c0 = hsl * kCW;                              // first column of this warp's slice
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    uint8_t* stg = staging + e * Cfg::kStagePerWarp;       // [2] x 4 KB boxes, [2] x 1 KB code blocks
+    const uint32_t stg_s = ptx::smem_u32(stg);
+    uint64_t* rb = rbars + 2 * e;
+    uint32_t rph[2] = {0u, 0u};
+    // lane l's 16-byte chunk c4 of its row in a SWIZZLE_128B 32 x 128 B box
+    auto sw = [lane](int c4) { return (uint32_t)(lane * 128 + ((c4 ^ (lane & 7)) << 4)); };
+    uint64_t* stats_g = reinterpret_cast<uint64_t*>(L.stats) + (size_t)group * (2 * np * 2 * BM);
+    const uint32_t dq_s = ptx::smem_u32(dq), ln_s = ptx::smem_u32(lnp);
+    if (lane == 0) {
+        ptx::tma_prefetch_desc(&lm.r);
+        ptx::tma_prefetch_desc(&lm.y);
+        if (L.qbits) ptx::tma_prefetch_desc(&lm.q);
+    }
+#ifdef MKQ_GTRACE
+    int gt_n = 0;
+#endif
+    auto load_res = [&](int tl, int ch) {   // TMA: residual box (tile tl, chunk ch) into buffer ch & 1
+        if (lane == 0 && tl < t_end) {
+            ptx::mbar_arrive_expect_tx(&rb[ch & 1], 4096);
+            ptx::tma_load_2d(&lm.r, &rb[ch & 1], stg + (ch & 1) * 4096, ncol0 + c0 + 32 * ch,
+                             tl * 2 * BM + rank * BM + q * 32);
+        }
+    };
+    int it = 0;
+    for (int tile = t_begin; tile < t_end; tile += t_step, ++it) {
+        const int ab = it & 1;
+        const uint32_t aph = (it >> 1) & 1;
+        const int mrow = tile * 2 * BM + rank * BM + q * 32;   // first row of this warp's 32
+        GTRACE(40);
+        // both boxes must have been read by the previous tile's output stores
+        if (lane == 0) ptx::tma_store_wait_read<0>();
+        __syncwarp();
+        load_res(tile, 0);
+        load_res(tile, 1);
+        ptx::mbar_wait_sleep<64>(&tfull[ab], aph);
+        GTRACE(42);
+        ptx::tc_fence_after();
+        float r[kCW];
+#pragma unroll
+        for (int ch = 0; ch < kCh; ++ch) {
+            uint32_t v[32];
+            ptx::tmem_ld_32x32b_x32(tmem_base + lane_off + ab * BN + c0 + 32 * ch, v);
+            ptx::tmem_ld_wait_regs(v);
+            GTRACE(52);
+            ptx::mbar_wait(&rb[ch & 1], rph[ch & 1]);
+            rph[ch & 1] ^= 1u;
+            GTRACE(53);
+#pragma unroll
+            for (int c4 = 0; c4 < 8; ++c4) {
+                const float4 rs = lds128f(stg_s + (ch & 1) * 4096 + sw(c4));
+#pragma unroll
+                for (int t = 0; t < 4; t += 2) {
+                    const int i = 4 * c4 + t;
+                    const float4 cp = lds128f(dq_s + 16u * (uint32_t)((c0 + 32 * ch + i) >> 1));   // (sc, sc', b, b')
+                    const int32_t a0 = fold ? (int32_t)v[i] : ((int32_t)v[i] >> 8);
+                    const int32_t a1 = fold ? (int32_t)v[i + 1] : ((int32_t)v[i + 1] >> 8);
+                    const float2 y = fma2(make_float2(__int2float_rn(a0), __int2float_rn(a1)), make_float2(cp.x, cp.y),
+                                          make_float2(cp.z, cp.w));
+                    const float2 rr = add2(y, t == 0 ? make_float2(rs.x, rs.y) : make_float2(rs.z, rs.w));
+                    r[32 * ch + i] = rr.x;
+                    r[32 * ch + i + 1] = rr.y;
+                }
+            }
+            if (ch + 2 < kCh) {   // this box is consumed: refill it with chunk ch + 2
+                ptx::fence_proxy_async_smem();
+                __syncwarp();
+                load_res(tile, ch + 2);
+            }
+        }
+        // the accumulator buffer is free for the MMA of tile it+2
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_remote(ptx::mapa(&tempty[ab], 0));
+        GTRACE(43);
+        // this warp's (mean, M2) over its kCW columns (4 f32x2 partial sums)
+        float2 sp[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+        for (int i = 0; i < kCW; i += 2) sp[(i >> 1) & 3] = add2(sp[(i >> 1) & 3], make_float2(r[i], r[i + 1]));
+        const float2 s2 = add2(add2(sp[0], sp[1]), add2(sp[2], sp[3]));
+        const float mw = __fdiv_rn(__fadd_rn(s2.x, s2.y), (float)kCW);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) sp[k] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int i = 0; i < kCW; i += 2) {
+            const float2 d = add2(make_float2(r[i], r[i + 1]), make_float2(-mw, -mw));
+            sp[(i >> 1) & 3] = fma2(d, d, sp[(i >> 1) & 3]);
+        }
+        const float2 m22 = add2(add2(sp[0], sp[1]), add2(sp[2], sp[3]));
+        const float m2 = __fadd_rn(m22.x, m22.y);
+        // combine: warps of the quadrant (CTA partial over BN columns), then the
+        // np CTAs of the row.  The CTA partial goes out as one 64-bit word
+        // (mean, M2 with its sign bit = this slot's use parity ^ 1), single-copy
+        // atomic: readers poll the words of their row until all np carry the
+        // current tag -- no fence, flag or counter.  M2 >= +0, so the sign bit is
+        // free; the slot starts zeroed (tag 0) and its first use writes tag 1.
+        qpart[hsl * BM + row_l] = make_float2(mw, m2);
+        GTRACE(44);
+        ptx::named_bar_sync(2 + q, 32 * kQW);
+        GTRACE(45);
+        uint64_t* slot = stats_g + (size_t)ab * np * (2 * BM);
+        const uint32_t tag = (((uint32_t)(it >> 1)) & 1u) ^ 1u;
+        if (hsl == 0) {
+            float2 c = qpart[row_l];
+#pragma unroll
+            for (int w = 1; w < kQW; ++w) {   // equal counts kCW: pairwise update
+                const float2 o = qpart[w * BM + row_l];
+                const float d = __fsub_rn(o.x, c.x);
+                const float nw = (float)(w * kCW), nt = (float)((w + 1) * kCW);
+                c.x = __fadd_rn(c.x, __fmul_rn(d, __fdiv_rn((float)kCW, nt)));
+                c.y = __fadd_rn(__fadd_rn(c.y, o.y), __fmul_rn(__fmul_rn(d, d), __fdiv_rn(nw * (float)kCW, nt)));
+            }
+            const uint64_t word = (uint64_t)__float_as_uint(c.x) | ((uint64_t)(__float_as_uint(c.y) | (tag << 31)) << 32);
+            st_relaxed_gpu_u64(slot + (size_t)j * (2 * BM) + rank * BM + row_l, word);
+        }
+        GTRACE(46);
+        float2 part[4];
+        {
+            const uint64_t* src = slot + rank * BM + row_l;
+            uint32_t pending = (1u << np) - 1u;
+            while (true) {
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) {
+                    if (jj < np && (pending >> jj & 1u)) {
+                        const uint64_t wv = ld_relaxed_gpu_u64(src + (size_t)jj * (2 * BM));
+                        if ((uint32_t)(wv >> 63) == tag) {
+                            part[jj] = make_float2(__uint_as_float((uint32_t)wv),
+                                                   __uint_as_float((uint32_t)(wv >> 32) & 0x7FFFFFFFu));
+                            pending &= ~(1u << jj);
+                        }
+                    }
+                }
+                if (!pending) break;
+                __nanosleep(20);
+            }
+        }
+        GTRACE(47);
+        float mean = part[0].x, M2 = part[0].y;
+#pragma unroll
+        for (int jj = 1; jj < 4; ++jj) {   // column tiles in order: pairwise update, counts BN
+            if (jj < np) {
+                const float d = __fsub_rn(part[jj].x, mean);
+                const float nw = (float)(jj * BN), nt = (float)((jj + 1) * BN);
+                mean = __fadd_rn(mean, __fmul_rn(d, __fdiv_rn((float)BN, nt)));
+                M2 = __fadd_rn(__fadd_rn(M2, part[jj].y), __fmul_rn(__fmul_rn(d, d), __fdiv_rn(nw * (float)BN, nt)));
+            }
+        }
+        const float rstd = rsqrtf(__fadd_rn(__fdiv_rn(M2, (float)N), L.eps));
+        // output: LN(r) staged per 32-column chunk in the swizzled boxes, TMA-stored
+#pragma unroll
+        for (int ch = 0; ch < kCh; ++ch) {
+            uint8_t* box = stg + (ch & 1) * 4096;
+            uint8_t* cbx = stg + 2 * 4096 + (ch & 1) * 1024;
+            GTRACE(50);
+            if (lane == 0) ptx::tma_store_wait_read<1>();   // the stores of chunk ch - 2 have read these
+            __syncwarp();
+            float o[32];
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) {
+                const float4 cp = lds128f(ln_s + 16u * (uint32_t)((c0 + 32 * ch + i) >> 1));   // (g, g', beta, beta')
+                const float2 d = add2(make_float2(r[32 * ch + i], r[32 * ch + i + 1]), make_float2(-mean, -mean));
+                const float2 oo = fma2(mul2(d, make_float2(rstd, rstd)), make_float2(cp.x, cp.y), make_float2(cp.z, cp.w));
+                o[i] = oo.x;
+                o[i + 1] = oo.y;
+            }
+#pragma unroll
+            for (int c4 = 0; c4 < 8; ++c4)
+                *reinterpret_cast<float4*>(box + sw(c4)) = make_float4(o[4 * c4], o[4 * c4 + 1], o[4 * c4 + 2], o[4 * c4 + 3]);
+            if (L.qbits == 4) {
+                uint32_t w[4];
+                bool near = false;
+#pragma unroll
+                for (int g8 = 0; g8 < 4; ++g8) {
+                    float v8[8];
+#pragma unroll
+                    for (int t = 0; t < 8; ++t) v8[t] = o[8 * g8 + t];
+                    w[g8] = quant_nib8_fast(v8, Qr, near);
+                }
+                if (__builtin_expect(near, 0)) {   // a value within 2^-18 of a rounding boundary
+#pragma unroll
+                    for (int g8 = 0; g8 < 4; ++g8)
+                        w[g8] = quant_nib8_exact(o[8 * g8], o[8 * g8 + 1], o[8 * g8 + 2], o[8 * g8 + 3], o[8 * g8 + 4],
+                                                 o[8 * g8 + 5], o[8 * g8 + 6], o[8 * g8 + 7], L.s_q, L.qmin, L.qmax);
+                }
+                *reinterpret_cast<uint4*>(cbx + lane * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+            } else if (L.qbits == 8) {
+                uint32_t w[8];
+#pragma unroll
+                for (int g4 = 0; g4 < 8; ++g4) w[g4] = quant_byte4_rcp(o[4 * g4], o[4 * g4 + 1], o[4 * g4 + 2], o[4 * g4 + 3], Qr);
+                *reinterpret_cast<uint4*>(cbx + lane * 32) = make_uint4(w[0], w[1], w[2], w[3]);
+                *reinterpret_cast<uint4*>(cbx + lane * 32 + 16) = make_uint4(w[4], w[5], w[6], w[7]);
+            }
+            ptx::fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+                ptx::tma_store_2d(&lm.y, box, ncol0 + c0 + 32 * ch, mrow);
+                if (L.qbits) ptx::tma_store_2d(&lm.q, cbx, (ncol0 + c0 + 32 * ch) * L.qbits / 8, mrow);
+                ptx::tma_store_commit();
+            }
+            GTRACE(51);
+        }
+        GTRACE(48);
+    }
+    if (lane == 0) ptx::tma_store_wait<0>();
+}
+
 template <class Cfg>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
     gemm_w4a4_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                          const __grid_constant__ CUtensorMap tmO, const Epi2Params p, int M, int N, int K) {
+                          const __grid_constant__ CUtensorMap tmO, const Epi2Params p, int M, int N, int K,
+                          const __grid_constant__ LnMaps lm) {
     constexpr int BM = Cfg::BM, BN = Cfg::BN, BNH = Cfg::BNH, S8 = Cfg::S8, SP = Cfg::SP;
     constexpr int kEpiThreads = 32 * Cfg::kEpiWarps;
     constexpr int kUnpThreads = 32 * Cfg::kUnpWarps;
@@ -403,6 +759,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
     uint64_t* tfull = emptyP + SP;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* rbars = tempty + 4;   // kLn: [kEpiWarps][2] residual TMA barriers (after the TMEM slot)
 
     const EpiParams& ep = p.e;
 #ifdef MKQ_GTRACE
@@ -415,8 +772,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
     const int nclusters = gridDim.x >> 1;
     const int m_tiles = (M + 2 * BM - 1) / (2 * BM);
     const int n_tiles = (N + BN - 1) / BN;
-    const int num_tiles = m_tiles * n_tiles;
     const int nk = (K + Cfg::BK - 1) / Cfg::BK;
+    // Tile schedule: tiles t_begin, t_begin + t_step, ... < t_end; tile -> output
+    // rows [tm0(t), +256) (this CTA: + rank*128) and columns [tn0(t), +BN).
+    // Default: pair `cluster` walks the (m, n) tiles.  kLn: the np pairs of a
+    // group take the np column tiles of the same row tiles (pairs past the
+    // last full group idle).
+    int t_begin = cluster, t_step = nclusters, t_end = m_tiles * n_tiles, ln_group = 0, ln_j = 0;
+    if constexpr (Cfg::kLn) {
+        const int np = p.ln.np, groups = nclusters / np;
+        ln_group = cluster / np;
+        ln_j = cluster % np;
+        t_begin = ln_group;
+        t_step = groups;
+        t_end = ln_group < groups ? m_tiles : 0;
+    }
+    auto tm0 = [&](int t) { return Cfg::kLn ? t * 2 * BM : (t / n_tiles) * 2 * BM; };
+    auto tn0 = [&](int t) { return Cfg::kLn ? ln_j * BN : (t % n_tiles) * BN; };
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < S8; ++i) {
@@ -431,8 +803,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(&tfull[i], 1);
             ptx::mbar_init(&tempty[i], 2 * Cfg::kEpiWarps);
-
         }
+        if constexpr (Cfg::kLn)
+            for (int i = 0; i < 2 * Cfg::kEpiWarps; ++i) ptx::mbar_init(&rbars[i], 1);
         ptx::fence_barrier_init();
     }
     if (warp == 0 && lane == 0) {
@@ -443,7 +816,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
     ptx::tc_fence_before();
     ptx::cluster_sync();
     __syncthreads();   // CTA barrier as well (orders the slot write for tools that do not model barrier.cluster)
-    ptx::pdl_launch();
+    // kLn CTAs wait on each other (row statistics): dependents are not released
+    // early, so a dependent grid can never hold SMs this grid still needs
+    if constexpr (!Cfg::kLn) ptx::pdl_launch();
     ptx::pdl_wait();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
@@ -451,15 +826,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
     // at one PC): producer/MMA group kRegProd, unpack kRegUnp, epilogue (the
     // latency-bound role) the rest of the launch allocation, kRegEpi
     if (warp < 4) {
-    if constexpr (Cfg::kLut4) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(Cfg::kRegProd));
+    if constexpr (Cfg::kRegSplit) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(Cfg::kRegProd));
     if (warp == 0) {
         // ---------------------------------------------------- TMA producer (both CTAs)
         if (lane == 0) {
             int s = 0;
             uint32_t ph = 0;
-            for (int tile = cluster; tile < num_tiles; tile += nclusters) {
-                const int m0 = (tile / n_tiles) * 2 * BM + (int)rank * BM;
-                const int n0 = (tile % n_tiles) * BN + (int)rank * BNH;
+            for (int tile = t_begin; tile < t_end; tile += t_step) {
+                const int m0 = tm0(tile) + (int)rank * BM;
+                const int n0 = tn0(tile) + (int)rank * BNH;
                 for (int kb = 0; kb < nk; ++kb) {
                     MKQ_WAIT_SLEEP(64, &emptyP[s], ph ^ 1);
                     uint8_t* dst = ringP + s * Cfg::kStageP;
@@ -480,7 +855,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
             int s = 0;
             uint32_t ph = 0;
             int it = 0;
-            for (int tile = cluster; tile < num_tiles; tile += nclusters, ++it) {
+            for (int tile = t_begin; tile < t_end; tile += t_step, ++it) {
                 const int ab = it & 1;
                 const uint32_t aph = (it >> 1) & 1;
                 GTRACE(29);
@@ -507,8 +882,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
         }
     }
     } else if (warp < 4 + Cfg::kEpiWarps) {
-        if constexpr (Cfg::kLut4) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(Cfg::kRegEpi));
+        if constexpr (Cfg::kRegSplit) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(Cfg::kRegEpi));
         // ---------------------------------------------------- epilogue (both CTAs)
+        if constexpr (Cfg::kLn) {
+            ln_epilogue<Cfg>(p, lm, tmem_base, tfull, tempty, rbars, staging, reinterpret_cast<float*>(scb), t_begin,
+                             t_step, t_end, ln_group, ln_j, M, N, (int)rank);
+        } else {
         const int e = warp - 4;           // 0..7
         const int q = warp & 3;           // TMEM lane quadrant (warp % 4)
         const int h = e >> 2;             // column part (kColsPerWarp columns)
@@ -548,23 +927,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
             for (int c = 0; c < kCW; ++c) {
                 const int n = (tl % n_tiles) * BN + h * Cfg::kColsPerWarp + 32 * c + lane;
                 float sw = 1.0f, bn = 0.0f;
-                if (tl < num_tiles && n < N) {
+                if (tl < t_end && n < N) {
                     sw = __ldg(ep.s_w + n);
                     bn = ep.bias ? __ldg(ep.bias + n) : 0.0f;
                 }
                 v2[c] = make_float2(sw, bn);
             }
         };
-        if constexpr (Cfg::kLut4) load_scales(cluster);
+        if constexpr (Cfg::kLut4) load_scales(t_begin);
         // this lane's replica of the compact table, and the same minus the cell
         // bias (bits(2^23) * 128 = 2^31 mod 2^32), held in vector registers
         const uint32_t tab = ptx::smem_u32(th) + 4u * (uint32_t)lane;
         const uint32_t tabm = lane_reg(tab - (rq::kMagic << 7));
         a4 = __uint_as_float(lane_reg(__float_as_uint(a4)));
         int it = 0;
-        for (int tile = cluster; tile < num_tiles; tile += nclusters, ++it) {
-            const int m0 = (tile / n_tiles) * 2 * BM + (int)rank * BM;
-            const int n0 = (tile % n_tiles) * BN;
+        for (int tile = t_begin; tile < t_end; tile += t_step, ++it) {
+            const int m0 = tm0(tile) + (int)rank * BM;
+            const int n0 = tn0(tile);
             const int ab = it & 1;
             const uint32_t aph = (it >> 1) & 1;
             float2* sb = scb + ab * BN;
@@ -590,7 +969,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
                     f[2] = v2[c].y;
                 }
                 __syncwarp();
-                load_scales(tile + nclusters);   // in flight during this tile
+                load_scales(tile + t_step);   // in flight during this tile
                 GTRACE(2);
                 // Accumulator wait.  Default: every warp sleeps between polls
                 // (test_wait + nanosleep): the suspend-hint try_wait wakes on every
@@ -722,8 +1101,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
             if (lane == 0) ptx::mbar_arrive_remote(ptx::mapa(&tempty[ab], 0));
         }
         if (lane == 0) ptx::tma_store_wait<0>();
+        }
     } else {
-        if constexpr (Cfg::kLut4) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(Cfg::kRegUnp));
+        if constexpr (Cfg::kRegSplit) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(Cfg::kRegUnp));
         // ---------------------------------------------------- int4 -> int8 unpack (both CTAs)
         const int u = threadIdx.x - 32 * (4 + Cfg::kEpiWarps);
         constexpr int kChunks = (BM + BNH) * (Cfg::BK / 32);   // 16-byte packed chunks per stage
@@ -739,7 +1119,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
         const uint32_t ringP_s = ptx::smem_u32(ringP), ring8_s = ptx::smem_u32(ring8);
         int sp = 0, s8 = 0;
         uint32_t php = 0, ph8 = 0;
-        for (int tile = cluster; tile < num_tiles; tile += nclusters) {
+        for (int tile = t_begin; tile < t_end; tile += t_step) {
             for (int kb = 0; kb < nk; ++kb) {
                 GTRACE(19);
                 MKQ_WAIT_SLEEP(32, &fullP[sp], php);

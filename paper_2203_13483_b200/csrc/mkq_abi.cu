@@ -276,9 +276,69 @@ mkq_status launch_gemm2(const void* a, int64_t lda, const void* w, int64_t ldw, 
     static const int max_cl = [] { const char* v = getenv("MKQ_MAX_CLUSTERS"); return v ? atoi(v) : 0; }();
     int clusters = tiles < sms / 2 ? tiles : sms / 2;
     if (max_cl > 0 && clusters > max_cl) clusters = max_cl;
+    mkq::LnMaps lm;   // unused outside the kLn epilogue
+    lm.r = lm.y = lm.q = ma;
     cudaError_t e = launch_k(mkq::gemm_w4a4_2cta_kernel<Cfg>, dim3(2 * clusters), dim3(Cfg::kThreads), Cfg::kSmem,
-                             st, 1, ma, mb, mo, ep, M, N, K);
+                             st, 1, ma, mb, mo, ep, M, N, K, lm);
     if (e != cudaSuccess) return cuda_fail(e, "gemm2 launch");
+    return MKQ_OK;
+}
+
+// Fused W4A4 GEMM + residual + LayerNorm (kLn; Gemm2Cfg<256, 8, 4, false, true>):
+// one persistent CTA pair per TPC, pairs grouped np at a time; row statistics
+// exchanged through `ws` (counters zeroed here, before the launch).
+using LnCfg = mkq::Gemm2Cfg<256, 8, 4, false, true>;
+int ln_groups(int sms, int np) { return (sms / 2) / np; }
+size_t ln_ws_bytes(int sms, int np) {
+    const int groups = ln_groups(sms, np);
+    return (size_t)groups * 2 * np * 256 * sizeof(uint64_t);
+}
+
+mkq_status launch_gemm2_ln(const void* a, int64_t lda, const void* w, int64_t ldw, int M, int N, int K,
+                           mkq::Epi2Params& ep, void* ws, int sms, cudaStream_t st) {
+    static bool attr_set[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!attr_set[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(mkq::gemm_w4a4_2cta_kernel<LnCfg>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, LnCfg::kSmem);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+        attr_set[dev] = true;
+    }
+    CUtensorMap ma, mb;
+    mkq_status s = make_map(&ma, a, (uint64_t)K / 2, (uint64_t)M, (uint64_t)lda, LnCfg::BK / 2, LnCfg::BM, false);
+    if (s != MKQ_OK) return s;
+    s = make_map(&mb, w, (uint64_t)K / 2, (uint64_t)N, (uint64_t)ldw, LnCfg::BK / 2, LnCfg::BNH, false);
+    if (s != MKQ_OK) return s;
+    const int np = N / 256;
+    const int groups = ln_groups(sms, np);
+    const int m_tiles = (M + 255) / 256;
+    const int g_used = groups < m_tiles ? groups : m_tiles;
+    ep.ln.flags = nullptr;
+    ep.ln.stats = static_cast<float*>(ws);
+    ep.ln.np = np;
+    mkq::LnMaps lm;
+    s = make_map_t(&lm.r, ep.ln.res, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (uint64_t)N, (uint64_t)M,
+                   (uint64_t)ep.ln.ldr * 4, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (s != MKQ_OK) return s;
+    s = make_map_t(&lm.y, ep.ln.y, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (uint64_t)N, (uint64_t)M, (uint64_t)ep.ln.ldy * 4,
+                   32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (s != MKQ_OK) return s;
+    lm.q = lm.r;
+    if (ep.ln.qbits) {
+        const uint64_t qb = (uint64_t)N * ep.ln.qbits / 8;
+        s = make_map_t(&lm.q, ep.ln.q, CU_TENSOR_MAP_DATA_TYPE_UINT8, qb, (uint64_t)M, (uint64_t)ep.ln.ldq,
+                       (uint32_t)(32 * ep.ln.qbits / 8), 32, CU_TENSOR_MAP_SWIZZLE_NONE);
+        if (s != MKQ_OK) return s;
+    }
+    // the statistics slots start at tag 0 (the first use writes tag 1)
+    cudaError_t e = cudaMemsetAsync(ws, 0, ln_ws_bytes(sms, np), st);
+    if (e != cudaSuccess) return cuda_fail(e, "statistics reset");
+    // every CTA is resident at once (one per SM, grid <= SM count): the row
+    // statistics wait on other pairs of the group
+    e = launch_k(mkq::gemm_w4a4_2cta_kernel<LnCfg>, dim3(2 * np * g_used), dim3(LnCfg::kThreads), LnCfg::kSmem, st, 1,
+                 ma, mb, ma, ep, M, N, K, lm);
+    if (e != cudaSuccess) return cuda_fail(e, "gemm_ln launch");
     return MKQ_OK;
 }
 
@@ -604,6 +664,49 @@ mkq_status mkq_gemm_w8a8(const void* a, int64_t lda, const void* w, int64_t ldw,
 void mkq_set_small_m_mode(int mode) { g_small_mode.store(mode < 0 ? -1 : (mode > 2 ? 2 : mode)); }
 
 size_t mkq_gemm_workspace_size(int64_t, int64_t, int64_t) { return 0; }
+
+size_t mkq_gemm_residual_ln_workspace_size(int64_t M, int64_t N) {
+    if (M <= 0 || N <= 0 || N % 256) return 0;
+    int sms = 148;
+    if (check_device(&sms) != MKQ_OK) sms = 148;
+    return ln_ws_bytes(sms, (int)(N / 256));
+}
+
+mkq_status mkq_gemm_residual_ln(const void* a, int64_t lda, const void* w, int64_t ldw, int64_t M, int64_t N,
+                                int64_t K, float s_a, const float* s_w, const float* bias, const float* res,
+                                int64_t ldr, const float* gamma, const float* beta, float eps, float* y, int64_t ldy,
+                                int q_bits, float s_q, int qmin, int qmax, void* q, int64_t ldq, void* ws,
+                                size_t ws_bytes, void* stream) {
+    if (M < 0 || N < 0 || K < 0) return fail(MKQ_ERR_SHAPE, "negative dimension");
+    if (M == 0) return MKQ_OK;
+    if (!a || !w || !s_w || !res || !gamma || !beta || !y || !ws) return fail(MKQ_ERR_NULL, "a, w, s_w, res, gamma, beta, y and ws are required");
+    if (q_bits && !q) return fail(MKQ_ERR_NULL, "q is required when q_bits != 0");
+    if (N % 256 || N < 256 || N > 1024) return fail(MKQ_ERR_SHAPE, "N must be 256, 512, 768 or 1024");
+    if (K <= 0 || K % 32 || K > MKQ_MAX_K) return fail(MKQ_ERR_SHAPE, "K must be a positive multiple of 32 <= %d", MKQ_MAX_K);
+    if (lda < K / 2 || ldw < K / 2 || lda % 16 || ldw % 16) return fail(MKQ_ERR_ALIGN, "lda/ldw: >= K/2 bytes, multiples of 16");
+    if (ldr < N || ldy < N || ldr % 4 || ldy % 4) return fail(MKQ_ERR_SHAPE, "ldr/ldy must be >= N and multiples of 4");
+    if (!aligned16(a) || !aligned16(w) || !aligned16(res) || !aligned16(y) || !aligned16(ws))
+        return fail(MKQ_ERR_ALIGN, "a, w, res, y and ws must be 16-byte aligned");
+    if (!finite_pos(s_a)) return fail(MKQ_ERR_SCALE, "s_a must be > 0 and finite");
+    if (!(eps >= 0.0f) || !std::isfinite(eps)) return fail(MKQ_ERR_SCALE, "eps must be finite and >= 0");
+    if (q_bits) {
+        if (q_bits != 4 && q_bits != 8) return fail(MKQ_ERR_RANGE, "q_bits must be 0, 4 or 8");
+        if (!finite_pos(s_q)) return fail(MKQ_ERR_SCALE, "s_q must be > 0 and finite");
+        if (!code_range_ok(q_bits, qmin, qmax)) return fail(MKQ_ERR_RANGE, "qmin/qmax");
+        if (ldq < (q_bits == 4 ? N / 2 : N) || ldq % 16 || !aligned16(q)) return fail(MKQ_ERR_ALIGN, "q rows: 16-byte aligned, ldq >= N*q_bits/8");
+    }
+    int sms = 0;
+    mkq_status st = check_device(&sms);
+    if (st != MKQ_OK) return st;
+    if (ws_bytes < ln_ws_bytes(sms, (int)(N / 256))) return fail(MKQ_ERR_WORKSPACE, "workspace too small");
+    mkq::Epi2Params p2{};
+    p2.e = mkq::EpiParams{mkq::OUT_F32, 0, s_a, s_w, bias, 1.0f, 0, 0, y, ldy * 4};
+    p2.table = nullptr;
+    p2.ln = mkq::Ln2Params{res, ldr, gamma, beta, eps, y, ldy, static_cast<uint8_t*>(q), ldq, q_bits, qmin, qmax,
+                           s_q, nullptr, nullptr, (int)(N / 256)};
+    PdlScope pdl_scope(M);
+    return launch_gemm2_ln(a, lda, w, ldw, (int)M, (int)N, (int)K, p2, ws, sms, static_cast<cudaStream_t>(stream));
+}
 
 size_t mkq_requant_table_size(void) { return mkq::rq::kTableBytes; }
 

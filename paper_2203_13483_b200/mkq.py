@@ -15,7 +15,7 @@ from ._lib import (OUT_BF16, OUT_F16, OUT_F32, OUT_I32, OUT_I4, OUT_I8, MkqEpilo
                    check, lib)
 
 __all__ = ["mkq_requant_table", "mkq_quantize_pack", "mkq_absmax_scale", "mkq_gemm_w4a4", "mkq_gemm_w8a8",
-           "mkq_attention", "mkq_residual_layernorm", "mkq_bert_layer", "mkq_interleave_blocks", "mkq_fake_quant",
+           "mkq_attention", "mkq_residual_layernorm", "mkq_bert_layer", "mkq_gemm_residual_ln", "mkq_interleave_blocks", "mkq_fake_quant",
            "mkq_act_scale", "mkq_attention_i8", "out_dtype_bytes",
            "OUT_F32", "OUT_BF16", "OUT_I32", "OUT_I4", "OUT_I8", "OUT_F16"]
 
@@ -189,6 +189,36 @@ def mkq_gemm_w8a8(a: torch.Tensor, w: torch.Tensor, s_a: float, s_w: torch.Tenso
     K = K if K is not None else a.shape[1]
     return _gemm("mkq_gemm_w8a8", a, w, K, s_a, s_w, bias, mode, gelu, s_out, qmin, qmax, out, stream,
                  requant_table)
+
+
+_LN_WS = {}
+
+
+def mkq_gemm_residual_ln(a: torch.Tensor, w: torch.Tensor, s_a: float, s_w: torch.Tensor,
+                         bias: Optional[torch.Tensor], res: torch.Tensor, gamma: torch.Tensor, beta: torch.Tensor,
+                         eps: float = 1e-12, K: Optional[int] = None, q_bits: int = 0, s_q: float = 1.0,
+                         qmin: int = -8, qmax: int = 7, y: Optional[torch.Tensor] = None,
+                         q: Optional[torch.Tensor] = None, stream=None):
+    """NEXT(4) fused glue: y = LN(W4A4 linear(a) + res) [+ Eq.1 codes of y]
+    (mkq_gemm_residual_ln; N = w rows = 256..1024 in steps of 256)."""
+    M, N = a.shape[0], w.shape[0]
+    K = K if K is not None else a.shape[1] * 2
+    if y is None:
+        y = torch.empty((M, N), dtype=torch.float32, device=a.device)
+    if q_bits and q is None:
+        q = torch.empty((M, N // 2 if q_bits == 4 else N), dtype=torch.uint8 if q_bits == 4 else torch.int8,
+                        device=a.device)
+    nb = int(lib().mkq_gemm_residual_ln_workspace_size(M, N))
+    key = (str(a.device), _stream(stream).value)
+    ws = _LN_WS.get(key)
+    if ws is None or ws.numel() < nb:
+        ws = torch.empty(max(nb, 16), dtype=torch.uint8, device=a.device)
+        _LN_WS[key] = ws
+    check("mkq_gemm_residual_ln", lib().mkq_gemm_residual_ln(
+        _ptr(a), _row_bytes(a), _ptr(w), _row_bytes(w), M, N, K, float(s_a), _ptr(s_w), _ptr(bias), _ptr(res),
+        res.stride(0), _ptr(gamma), _ptr(beta), float(eps), _ptr(y), y.stride(0), int(q_bits), float(s_q),
+        qmin, qmax, _ptr(q), 0 if q is None else _row_bytes(q), _ptr(ws), ws.numel(), _stream(stream)))
+    return (y, q) if q_bits else y
 
 
 def mkq_attention(qkv: torch.Tensor, heads: int, batch: int, max_seq: int,
