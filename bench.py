@@ -158,8 +158,10 @@ def setup_layer(torch, dev, rank):
 
 
 def stage_calls(M, L, h_in, B, T, stream):
-    """The eight launches of mkq_bert_layer as separate C-ABI calls (same
-    kernels, same arguments) so each can be bracketed by CUDA events."""
+    """The launches of mkq_bert_layer as separate C-ABI calls (same kernels,
+    same arguments) so each can be bracketed by CUDA events: eight stages, or
+    six when the layer fuses residual + LayerNorm into the W^A and W^2 GEMMs
+    (mkq_gemm_residual_ln, NEXT(4); L.fused_ln(T))."""
     import torch
     hd, F, bits = L.hidden, L.ffn, L.bits
     t = L.t
@@ -195,6 +197,18 @@ def stage_calls(M, L, h_in, B, T, stream):
         ("ln2", lambda: M.mkq_residual_layernorm(buf["f"], buf["h1"], t["ln2_g"], t["ln2_b"], L.ln_eps,
                                                  y=buf["out"], stream=stream), 0),
     ]
+    if L.fused_ln(T):
+        fused = {
+            "gemm_o_ln1": (lambda: M.mkq_gemm_residual_ln(
+                buf["c_oa"], t["w_o"], s["s_o_in"], t["sw_o"], t["b_o"], h_in, t["ln1_g"], t["ln1_b"], L.ln_eps, K=hd,
+                q_bits=4, s_q=s["s_ffn1_in"], y=buf["h1"], q=buf["c_h1"], stream=stream), 2.0 * T * hd * hd),
+            "gemm_ffn2_ln2": (lambda: M.mkq_gemm_residual_ln(
+                buf["a2"], t["w_2"], s["s_ffn2_in"], t["sw_2"], t["b_2"], buf["h1"], t["ln2_g"], t["ln2_b"], L.ln_eps,
+                K=F, y=buf["out"], stream=stream), 2.0 * T * hd * F),
+        }
+        calls = [c for c in calls if c[0] not in ("gemm_o", "ln1_quant", "gemm_ffn2", "ln2")]
+        calls.insert(3, ("gemm_o_ln1",) + fused["gemm_o_ln1"])
+        calls.append(("gemm_ffn2_ln2",) + fused["gemm_ffn2_ln2"])
     return calls, buf
 
 
@@ -222,6 +236,9 @@ def stage_bytes(T, hd, F):
         "gemm_ffn1": T * hd / 2 + F * hd / 2 + T * F / 2,
         "gemm_ffn2": T * F / 2 + F * hd / 2 + T * hd * 4,
         "ln2": T * hd * 12,
+        # fused residual + LN (NEXT(4)): codes + weights + residual in, y (+ codes) out
+        "gemm_o_ln1": T * hd / 2 + hd * hd / 2 + T * hd * 4 + T * hd * 4 + T * hd / 2,
+        "gemm_ffn2_ln2": T * F / 2 + F * hd / 2 + T * hd * 4 + T * hd * 4,
     }
 
 
@@ -492,7 +509,7 @@ def run_ours(args):
                     "d2h_bytes_per_step": int(h_host.nbytes),
                     "pipeline": f"{nch} chunks of {Bc} sequences per rank over H2D / compute / D2H streams",
                     "result_equals_device_step": e2e_same},
-            "gpu_launches": 8 * args.steps,
+            "gpu_launches": len(stage_ms) * args.steps,
             "clocks": clocks,
             "cpu_baseline": cpu,
             "c3_row_sharded": c3_rs,

@@ -333,6 +333,11 @@ typedef struct {
     int32_t out_bits;
 } mkq_layer;
 
+/* 1 if mkq_bert_layer runs the W^A + LN1 and W^2 + LN2 stages as
+ * mkq_gemm_residual_ln (W4A4, hidden in {256, 512, 768, 1024}, tokens >=
+ * 4096), 0 if as mkq_gemm_w4a4/w8a8 + mkq_residual_layernorm. */
+MKQ_API int mkq_layer_fused_ln(const mkq_layer *L, int64_t tokens);
+
 /* Workspace bytes for `tokens` rows (intermediates of one layer). */
 MKQ_API size_t mkq_bert_layer_workspace_size(const mkq_layer *L, int64_t tokens);
 

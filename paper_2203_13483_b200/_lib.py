@@ -45,6 +45,7 @@ SIGNATURES = {
     "mkq_act_scale_workspace_size": (SZ, []),
     "mkq_act_scale": (I32, [P, I64, ctypes.c_double, F32, P, P, SZ, P]),
     "mkq_bert_layer_workspace_size": (SZ, [P, I64]),
+    "mkq_layer_fused_ln": (I32, [P, I64]),
     "mkq_bert_layer": (I32, [P, P, I64, I64, P, I64, P, P, SZ, P]),
 }
 

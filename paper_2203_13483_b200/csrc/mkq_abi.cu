@@ -1100,27 +1100,41 @@ mkq_status mkq_act_scale(const float* x, int64_t n, double p, float l_max, float
 }
 
 // ------------------------------------------------------------------ BERT layer
+// Does the layer run its residual + LayerNorm stages fused into the GEMMs
+// (mkq_gemm_residual_ln: W^A + LN1, W^2 + LN2)?  W4A4 layers with hidden in
+// {256, 512, 768, 1024} and at least 4096 tokens (below that the small-M GEMM
+// plans and the standalone LN kernels are faster).
+static bool layer_fused_ln(const mkq_layer* L, int64_t T) {
+    return L->bits == 4 && L->hidden % 256 == 0 && L->hidden <= 1024 && T >= 4096;
+}
+
 struct LayerWs {
-    size_t codes_in, qkv, codes_oa, o, h1, codes_h1, codes_ffn2, f, total;
+    size_t codes_in, qkv, codes_oa, o, h1, codes_h1, codes_ffn2, f, ln, total;
 };
 
 static LayerWs layer_ws(const mkq_layer* L, int64_t T) {
     LayerWs w;
     const int64_t h = L->hidden, F = L->ffn;
     const int64_t cb = L->bits == 4 ? 1 : 2;   // code bytes per 2 elements
+    const bool fused = layer_fused_ln(L, T);
     size_t off = 0;
     auto take = [&](size_t bytes) { size_t o = off; off += align256(bytes); return o; };
     w.codes_in = take((size_t)T * h * cb / 2);
     w.qkv = take((size_t)T * 3 * h * 2);
     w.codes_oa = take((size_t)T * h * cb / 2);
-    w.o = take((size_t)T * h * 4);
+    w.o = fused ? 0 : take((size_t)T * h * 4);
     w.h1 = take((size_t)T * h * 4);
     w.codes_h1 = take((size_t)T * h * cb / 2);
     w.codes_ffn2 = take((size_t)T * F * cb / 2);
-    w.f = take((size_t)T * h * 4);
+    w.f = fused ? 0 : take((size_t)T * h * 4);
+    int sms = 148;
+    if (fused && check_device(&sms) != MKQ_OK) sms = 148;
+    w.ln = fused ? take(ln_ws_bytes(sms, (int)(h / 256))) : 0;
     w.total = off;
     return w;
 }
+
+int mkq_layer_fused_ln(const mkq_layer* L, int64_t tokens) { return L && layer_fused_ln(L, tokens) ? 1 : 0; }
 
 size_t mkq_bert_layer_workspace_size(const mkq_layer* L, int64_t tokens) {
     if (!L || tokens < 0) return 0;
@@ -1204,25 +1218,43 @@ mkq_status mkq_bert_layer(const mkq_layer* L, const float* h_in, int64_t batch, 
         MKQ_TRY(mkq_attention(qkv, 3 * h, batch, max_seq, cu, T, L->heads, 64, bits == 4 ? MKQ_OUT_I4 : MKQ_OUT_I8,
                               L->s_o_in, qlo, qhi, codes_oa, cbh, stream));
     }
-    // W^A projection (+ b^A) -> fp32
+    const bool fused_ln = layer_fused_ln(L, T);
+    void* ln_ws = base + W.ln;
+    const size_t ln_bytes = fused_ln ? ln_ws_bytes(sms, (int)(h / 256)) : 0;
     mkq_epilogue e_f32{MKQ_OUT_F32, 0, 1.0f, 0, 0, nullptr};
-    MKQ_TRY(gemm(codes_oa, cbh, L->w_o, cbh, T, h, h, L->s_o_in, L->sw_o, L->b_o, &e_f32, o, h * 4, nullptr, 0,
-                 stream));
-    // LN1(o + h) -> h1 fp32 and its codes for FFN1 (fused a1)
-    MKQ_TRY(mkq_residual_layernorm(o, h_in, T, h, h, L->ln1_g, L->ln1_b, L->ln_eps, h1, bits, L->s_ffn1_in, qlo,
-                                   qhi, codes_h1, cbh, stream));
+    if (fused_ln) {
+        // W^A projection + residual + LN1 -> h1 fp32 and its codes for FFN1, one kernel (NEXT(4))
+        MKQ_TRY(mkq_gemm_residual_ln(codes_oa, cbh, L->w_o, cbh, T, h, h, L->s_o_in, L->sw_o, L->b_o, h_in, h,
+                                     L->ln1_g, L->ln1_b, L->ln_eps, h1, h, 4, L->s_ffn1_in, qlo, qhi, codes_h1, cbh,
+                                     ln_ws, ln_bytes, stream));
+    } else {
+        // W^A projection (+ b^A) -> fp32
+        MKQ_TRY(gemm(codes_oa, cbh, L->w_o, cbh, T, h, h, L->s_o_in, L->sw_o, L->b_o, &e_f32, o, h * 4, nullptr, 0,
+                     stream));
+        // LN1(o + h) -> h1 fp32 and its codes for FFN1 (fused a1)
+        MKQ_TRY(mkq_residual_layernorm(o, h_in, T, h, h, L->ln1_g, L->ln1_b, L->ln_eps, h1, bits, L->s_ffn1_in, qlo,
+                                       qhi, codes_h1, cbh, stream));
+    }
     // FFN1: GELU + requantize to the FFN2 input codes (a5, a6 fused)
     mkq_epilogue e_ffn1{bits == 4 ? MKQ_OUT_I4 : MKQ_OUT_I8, 1, L->s_ffn2_in, qlo, qhi, L->ffn1_requant_table};
     MKQ_TRY(gemm(codes_h1, cbh, L->w_1, cbh, T, F, h, L->s_ffn1_in, L->sw_1, L->b_1, &e_ffn1, codes_ffn2, cbf,
                  nullptr, 0, stream));
-    // FFN2 -> fp32
-    MKQ_TRY(gemm(codes_ffn2, cbf, L->w_2, cbf, T, h, F, L->s_ffn2_in, L->sw_2, L->b_2, &e_f32, f, h * 4, nullptr,
-                 0, stream));
-    // LN2(f + h1) -> h_out (+ the next layer's input codes, fused a1)
     const int ob = L->out_codes ? L->out_bits : 0;
-    MKQ_TRY(mkq_residual_layernorm(f, h1, T, h, h, L->ln2_g, L->ln2_b, L->ln_eps, h_out, ob,
-                                   ob ? L->s_out_codes : 1.0f, ob == 4 ? -8 : -128, ob == 4 ? 7 : 127, L->out_codes,
-                                   ob == 4 ? h / 2 : h, stream));
+    if (fused_ln) {
+        // FFN2 + residual + LN2 -> h_out (+ the next layer's input codes), one kernel (NEXT(4))
+        MKQ_TRY(mkq_gemm_residual_ln(codes_ffn2, cbf, L->w_2, cbf, T, h, F, L->s_ffn2_in, L->sw_2, L->b_2, h1, h,
+                                     L->ln2_g, L->ln2_b, L->ln_eps, h_out, h, ob, ob ? L->s_out_codes : 1.0f,
+                                     ob == 4 ? -8 : -128, ob == 4 ? 7 : 127, L->out_codes, ob == 4 ? h / 2 : h, ln_ws,
+                                     ln_bytes, stream));
+    } else {
+        // FFN2 -> fp32
+        MKQ_TRY(gemm(codes_ffn2, cbf, L->w_2, cbf, T, h, F, L->s_ffn2_in, L->sw_2, L->b_2, &e_f32, f, h * 4, nullptr,
+                     0, stream));
+        // LN2(f + h1) -> h_out (+ the next layer's input codes, fused a1)
+        MKQ_TRY(mkq_residual_layernorm(f, h1, T, h, h, L->ln2_g, L->ln2_b, L->ln_eps, h_out, ob,
+                                       ob ? L->s_out_codes : 1.0f, ob == 4 ? -8 : -128, ob == 4 ? 7 : 127,
+                                       L->out_codes, ob == 4 ? h / 2 : h, stream));
+    }
 #undef MKQ_TRY
     return MKQ_OK;
 }

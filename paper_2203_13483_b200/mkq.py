@@ -316,6 +316,10 @@ class QLayer:
     def workspace_size(self, tokens: int) -> int:
         return int(lib().mkq_bert_layer_workspace_size(ctypes.byref(self.c), tokens))
 
+    def fused_ln(self, tokens: int) -> bool:
+        """mkq_bert_layer runs W^A + LN1 and W^2 + LN2 as mkq_gemm_residual_ln."""
+        return bool(lib().mkq_layer_fused_ln(ctypes.byref(self.c), tokens))
+
 
 def mkq_bert_layer(layer: QLayer, h_in: torch.Tensor, batch: int, max_seq: int,
                    cu_seqlens: Optional[torch.Tensor] = None, h_out: Optional[torch.Tensor] = None,

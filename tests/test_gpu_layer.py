@@ -252,8 +252,14 @@ def _stagewise_sampled(L, W, h, B, S, seqlens, cu_d, seqs):
     o_g = gemm(c_oa, t["w_o"], sc["s_o_in"], t["sw_o"], t["b_o"], mode=M.OUT_F32, K=hidden)
     o = host(o_g)
     assert np.array_equal(o[rows], oracle.linear(codes_oa, W.o.codes, W.s_o_in, W.o.s_w, W.o.bias))
-    h1_g, c_h1 = M.mkq_residual_layernorm(o_g, hd, t["ln1_g"], t["ln1_b"], 1e-12, bits=bits, s_q=sc["s_ffn1_in"],
-                                          qmin=lo, qmax=hi)
+    fused = L.fused_ln(T)   # the layer runs W^A + LN1 and W^2 + LN2 as mkq_gemm_residual_ln (NEXT(4))
+    if fused:
+        h1_g, c_h1 = M.mkq_gemm_residual_ln(c_oa, t["w_o"], sc["s_o_in"], t["sw_o"], t["b_o"], hd, t["ln1_g"],
+                                            t["ln1_b"], 1e-12, K=hidden, q_bits=bits, s_q=sc["s_ffn1_in"], qmin=lo,
+                                            qmax=hi)
+    else:
+        h1_g, c_h1 = M.mkq_residual_layernorm(o_g, hd, t["ln1_g"], t["ln1_b"], 1e-12, bits=bits,
+                                              s_q=sc["s_ffn1_in"], qmin=lo, qmax=hi)
     h1 = host(h1_g)
     ref_h1 = OL.layernorm(o[rows].astype(np.float64) + h[rows], W.ln1_g, W.ln1_b)
     assert np.abs(h1[rows] - ref_h1).max() < 2e-5 * max(1.0, np.abs(ref_h1).max())
@@ -268,7 +274,11 @@ def _stagewise_sampled(L, W, h, B, S, seqlens, cu_d, seqs):
     f_g = gemm(a2, t["w_2"], sc["s_ffn2_in"], t["sw_2"], t["b_2"], mode=M.OUT_F32, K=ffn)
     f = host(f_g)
     assert np.array_equal(f[rows], oracle.linear(ref_a2, W.w2.codes, W.s_ffn2_in, W.w2.s_w, W.w2.bias))
-    y = host(M.mkq_residual_layernorm(f_g, h1_g, t["ln2_g"], t["ln2_b"], 1e-12))
+    if fused:
+        y = host(M.mkq_gemm_residual_ln(a2, t["w_2"], sc["s_ffn2_in"], t["sw_2"], t["b_2"], h1_g, t["ln2_g"],
+                                        t["ln2_b"], 1e-12, K=ffn))
+    else:
+        y = host(M.mkq_residual_layernorm(f_g, h1_g, t["ln2_g"], t["ln2_b"], 1e-12))
     ref_y = OL.layernorm(f[rows].astype(np.float64) + h1[rows], W.ln2_g, W.ln2_b)
     assert np.abs(y[rows] - ref_y).max() < 2e-5 * max(1.0, np.abs(ref_y).max())
     assert np.array_equal(y, out)   # the fused layer runs exactly these kernels
