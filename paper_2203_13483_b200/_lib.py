@@ -84,6 +84,8 @@ def lib() -> ctypes.CDLL:
                 "(there is no fallback implementation)")
         L = ctypes.CDLL(SO)
         for name, (res, args) in SIGNATURES.items():
+            if os.environ.get("MKQ_LIB") and not hasattr(L, name):
+                continue   # diagnostics: an older build selected with MKQ_LIB may lack newer entry points
             f = getattr(L, name)
             f.restype = res
             f.argtypes = args

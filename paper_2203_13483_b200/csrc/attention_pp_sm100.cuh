@@ -426,7 +426,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                         float v[8];
 #pragma unroll
                         for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(o[gq >> 2][8 * (gq & 3) + i]) * inv;
-                        wq[gq] = quant_nib8_rcp(v, Q);
+                        bool near = false;
+                        wq[gq] = quant_nib8_fast(v, Q, near);
+                        if (__builtin_expect(near, 0))   // within 2^-18 of a rounding boundary: exact Eq.1
+                            wq[gq] = quant_nib8_exact(v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7], p.s_out, p.qmin,
+                                                      p.qmax);
                     }
                     TRACE(9);
                     uint4* dst = reinterpret_cast<uint4*>(orow + I.head * kD / 2);

@@ -92,6 +92,54 @@ __device__ __forceinline__ uint32_t quant_byte4_rcp(float v0, float v1, float v2
     return (uint32_t)(c0 & 0xFF) | ((uint32_t)(c1 & 0xFF) << 8) | ((uint32_t)(c2 & 0xFF) << 16) | ((uint32_t)(c3 & 0xFF) << 24);
 }
 
+// f32x2 arithmetic (sm_100: two IEEE RN fp32 operations per instruction)
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {   // two IEEE RN fmas, one instruction
+    uint64_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;"
+        : "=l"(r)
+        : "l"(*reinterpret_cast<const uint64_t*>(&a)), "l"(*reinterpret_cast<const uint64_t*>(&b)),
+          "l"(*reinterpret_cast<const uint64_t*>(&c)));
+    return *reinterpret_cast<float2*>(&r);
+}
+
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {   // two IEEE RN adds, one instruction
+    uint64_t r;
+    asm("add.rn.f32x2 %0, %1, %2;"
+        : "=l"(r)
+        : "l"(*reinterpret_cast<const uint64_t*>(&a)), "l"(*reinterpret_cast<const uint64_t*>(&b)));
+    return *reinterpret_cast<float2*>(&r);
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {   // two IEEE RN multiplies, one instruction
+    uint64_t r;
+    asm("mul.rn.f32x2 %0, %1, %2;"
+        : "=l"(r)
+        : "l"(*reinterpret_cast<const uint64_t*>(&a)), "l"(*reinterpret_cast<const uint64_t*>(&b)));
+    return *reinterpret_cast<float2*>(&r);
+}
+
+// Eq.1 codes of 8 values with one scale, int4 nibbles packed (value i in
+// nibble i), for epilogues where |code| is small: q = fl(x * RN(1/s)) differs
+// from fl(x / s) by at most 2 ulps of |q| <= 2^-19 inside the code range
+// [qmin, qmax] (|q| <= 8 after the clamp), so rint(clamp(q)) equals Eq.1's
+// rint(clamp(fl(x/s))) unless q lies within 2^-18 of a half-integer, which the
+// caller's `near` reports (evaluate those groups with quant_code).  Clamping
+// before rounding is rounding before clamping for integer bounds.
+__device__ __forceinline__ uint32_t quant_nib8_fast(const float (&x)[8], const QuantRcp& Q, bool& near) {
+    uint32_t w = 0;
+#pragma unroll
+    for (int i = 0; i < 8; i += 2) {
+        float2 q = mul2(make_float2(x[i], x[i + 1]), make_float2(Q.r, Q.r));
+        q.x = fminf(fmaxf(q.x, Q.lo), Q.hi);
+        q.y = fminf(fmaxf(q.y, Q.lo), Q.hi);
+        const float2 t = add2(q, make_float2(12582912.0f, 12582912.0f));
+        const float2 d = fma2(add2(t, make_float2(-12582912.0f, -12582912.0f)), make_float2(-1.0f, -1.0f), q);
+        near |= fabsf(fabsf(d.x) - 0.5f) <= 0x1p-18f;
+        near |= fabsf(fabsf(d.y) - 0.5f) <= 0x1p-18f;
+        w |= ((__float_as_uint(t.x) & 0xFu) << (4 * i)) | ((__float_as_uint(t.y) & 0xFu) << (4 * i + 4));
+    }
+    return w;
+}
+
 // Dequant (P:66 s*q, P:93/P:98 bias; reading R4).
 __device__ __forceinline__ float dequant(int32_t acc, float sc, float b, bool has_bias) {
     float a = __int2float_rn(acc);

@@ -300,53 +300,6 @@ __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
     return v;
 }
 
-__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {   // two IEEE RN fmas, one instruction
-    uint64_t r;
-    asm("fma.rn.f32x2 %0, %1, %2, %3;"
-        : "=l"(r)
-        : "l"(*reinterpret_cast<const uint64_t*>(&a)), "l"(*reinterpret_cast<const uint64_t*>(&b)),
-          "l"(*reinterpret_cast<const uint64_t*>(&c)));
-    return *reinterpret_cast<float2*>(&r);
-}
-
-__device__ __forceinline__ float2 add2(float2 a, float2 b) {   // two IEEE RN adds, one instruction
-    uint64_t r;
-    asm("add.rn.f32x2 %0, %1, %2;"
-        : "=l"(r)
-        : "l"(*reinterpret_cast<const uint64_t*>(&a)), "l"(*reinterpret_cast<const uint64_t*>(&b)));
-    return *reinterpret_cast<float2*>(&r);
-}
-__device__ __forceinline__ float2 mul2(float2 a, float2 b) {   // two IEEE RN multiplies, one instruction
-    uint64_t r;
-    asm("mul.rn.f32x2 %0, %1, %2;"
-        : "=l"(r)
-        : "l"(*reinterpret_cast<const uint64_t*>(&a)), "l"(*reinterpret_cast<const uint64_t*>(&b)));
-    return *reinterpret_cast<float2*>(&r);
-}
-
-// Eq.1 codes of 8 values with one scale, int4 nibbles packed (value i in
-// nibble i), for epilogues where |code| is small: q = fl(x * RN(1/s)) differs
-// from fl(x / s) by at most 2 ulps of |q| <= 2^-19 inside the code range
-// [qmin, qmax] (|q| <= 8 after the clamp), so rint(clamp(q)) equals Eq.1's
-// rint(clamp(fl(x/s))) unless q lies within 2^-18 of a half-integer, which the
-// caller's `near` reports (evaluate those groups with quant_code).  Clamping
-// before rounding is rounding before clamping for integer bounds.
-__device__ __forceinline__ uint32_t quant_nib8_fast(const float (&x)[8], const QuantRcp& Q, bool& near) {
-    uint32_t w = 0;
-#pragma unroll
-    for (int i = 0; i < 8; i += 2) {
-        float2 q = mul2(make_float2(x[i], x[i + 1]), make_float2(Q.r, Q.r));
-        q.x = fminf(fmaxf(q.x, Q.lo), Q.hi);
-        q.y = fminf(fmaxf(q.y, Q.lo), Q.hi);
-        const float2 t = add2(q, make_float2(12582912.0f, 12582912.0f));
-        const float2 d = fma2(add2(t, make_float2(-12582912.0f, -12582912.0f)), make_float2(-1.0f, -1.0f), q);
-        near |= fabsf(fabsf(d.x) - 0.5f) <= 0x1p-18f;
-        near |= fabsf(fabsf(d.y) - 0.5f) <= 0x1p-18f;
-        w |= ((__float_as_uint(t.x) & 0xFu) << (4 * i)) | ((__float_as_uint(t.y) & 0xFu) << (4 * i + 4));
-    }
-    return w;
-}
-
 // A register the compiler cannot prove warp-uniform or constant: keeps values
 // used by every output in one vector register (a uniform value feeding an FFMA
 // that already takes a uniform operand is otherwise re-copied per use, and a
@@ -735,11 +688,11 @@ __device__ __forceinline__ void ln_epilogue(const Epi2Params& p, const LnMaps& l
     if (lane == 0) ptx::tma_store_wait<0>();
 }
 
+// The kernel body, shared by gemm_w4a4_2cta_kernel (plain epilogues) and
+// gemm_w4a4_ln_kernel (kLn); `lm` is dereferenced only by the kLn epilogue.
 template <class Cfg>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
-    gemm_w4a4_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                          const __grid_constant__ CUtensorMap tmO, const Epi2Params p, int M, int N, int K,
-                          const __grid_constant__ LnMaps lm) {
+__device__ __forceinline__ void gemm2_body(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmO,
+                                           const Epi2Params& p, int M, int N, int K, const LnMaps* lmp) {
     constexpr int BM = Cfg::BM, BN = Cfg::BN, BNH = Cfg::BNH, S8 = Cfg::S8, SP = Cfg::SP;
     constexpr int kEpiThreads = 32 * Cfg::kEpiWarps;
     constexpr int kUnpThreads = 32 * Cfg::kUnpWarps;
@@ -885,7 +838,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
         if constexpr (Cfg::kRegSplit) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(Cfg::kRegEpi));
         // ---------------------------------------------------- epilogue (both CTAs)
         if constexpr (Cfg::kLn) {
-            ln_epilogue<Cfg>(p, lm, tmem_base, tfull, tempty, rbars, staging, reinterpret_cast<float*>(scb), t_begin,
+            ln_epilogue<Cfg>(p, *lmp, tmem_base, tfull, tempty, rbars, staging, reinterpret_cast<float*>(scb), t_begin,
                              t_step, t_end, ln_group, ln_j, M, N, (int)rank);
         } else {
         const int e = warp - 4;           // 0..7
@@ -1174,6 +1127,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
         ptx::tc_fence_after();
         ptx::tmem_dealloc_2cta<Cfg::kTmemCols>(tmem_base);
     }
+}
+
+template <class Cfg>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
+    gemm_w4a4_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                          const __grid_constant__ CUtensorMap tmO, const Epi2Params p, int M, int N, int K) {
+    static_assert(!Cfg::kLn, "kLn: gemm_w4a4_ln_kernel");
+    gemm2_body<Cfg>(tmA, tmB, tmO, p, M, N, K, nullptr);
+}
+
+template <class Cfg>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
+    gemm_w4a4_ln_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                        const Epi2Params p, int M, int N, int K, const __grid_constant__ LnMaps lm) {
+    static_assert(Cfg::kLn, "plain epilogues: gemm_w4a4_2cta_kernel");
+    gemm2_body<Cfg>(tmA, tmB, tmA, p, M, N, K, &lm);
 }
 
 }  // namespace mkq

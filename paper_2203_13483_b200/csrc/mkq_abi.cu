@@ -276,10 +276,8 @@ mkq_status launch_gemm2(const void* a, int64_t lda, const void* w, int64_t ldw, 
     static const int max_cl = [] { const char* v = getenv("MKQ_MAX_CLUSTERS"); return v ? atoi(v) : 0; }();
     int clusters = tiles < sms / 2 ? tiles : sms / 2;
     if (max_cl > 0 && clusters > max_cl) clusters = max_cl;
-    mkq::LnMaps lm;   // unused outside the kLn epilogue
-    lm.r = lm.y = lm.q = ma;
     cudaError_t e = launch_k(mkq::gemm_w4a4_2cta_kernel<Cfg>, dim3(2 * clusters), dim3(Cfg::kThreads), Cfg::kSmem,
-                             st, 1, ma, mb, mo, ep, M, N, K, lm);
+                             st, 1, ma, mb, mo, ep, M, N, K);
     if (e != cudaSuccess) return cuda_fail(e, "gemm2 launch");
     return MKQ_OK;
 }
@@ -300,7 +298,7 @@ mkq_status launch_gemm2_ln(const void* a, int64_t lda, const void* w, int64_t ld
     int dev = 0;
     cudaGetDevice(&dev);
     if (!attr_set[dev]) {
-        cudaError_t e = cudaFuncSetAttribute(mkq::gemm_w4a4_2cta_kernel<LnCfg>,
+        cudaError_t e = cudaFuncSetAttribute(mkq::gemm_w4a4_ln_kernel<LnCfg>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, LnCfg::kSmem);
         if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
         attr_set[dev] = true;
@@ -336,8 +334,8 @@ mkq_status launch_gemm2_ln(const void* a, int64_t lda, const void* w, int64_t ld
     if (e != cudaSuccess) return cuda_fail(e, "statistics reset");
     // every CTA is resident at once (one per SM, grid <= SM count): the row
     // statistics wait on other pairs of the group
-    e = launch_k(mkq::gemm_w4a4_2cta_kernel<LnCfg>, dim3(2 * np * g_used), dim3(LnCfg::kThreads), LnCfg::kSmem, st, 1,
-                 ma, mb, ma, ep, M, N, K, lm);
+    e = launch_k(mkq::gemm_w4a4_ln_kernel<LnCfg>, dim3(2 * np * g_used), dim3(LnCfg::kThreads), LnCfg::kSmem, st, 1,
+                 ma, mb, ep, M, N, K, lm);
     if (e != cudaSuccess) return cuda_fail(e, "gemm_ln launch");
     return MKQ_OK;
 }
