@@ -43,7 +43,7 @@ def main():
         torch.cuda.synchronize()
         torch.cuda.profiler.stop()
     else:
-        calls, _ = bench.stage_calls(M, L, h_in, ws, T, stream)
+        calls, _ = bench.stage_calls(M, L, h_in, B, T, stream)
         for c in calls:       # warm-up pass
             c[1]()
         torch.cuda.synchronize()

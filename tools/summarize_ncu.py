@@ -89,7 +89,7 @@ def main():
     os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
     with open(a.out + "_kernels.md", "w") as f:
         f.write(f"# ncu --set full summary ({os.path.basename(a.rep)})\n\n")
-        f.write("One launch of each of the eight kernels of the BERT-large W4A4 layer step (bench.py workload,\n"
+        f.write(f"One launch of each of the {len(labels)} kernels of the BERT-large W4A4 layer step (bench.py workload,\n"
                 "tools/prof_layer.py), `ncu --set full --clock-control none`.  Durations are ncu's serialised,\n"
                 "cold-cache replays: compare shares, not absolutes, with bench.py's live CUDA-event times.\n\n")
         f.write("\n".join(lines) + "\n")

@@ -25,7 +25,7 @@ Bn, S, hd = bench.CFG["batch"], bench.CFG["seq"], bench.CFG["hidden"]
 T = Bn * S
 h_in = torch.from_numpy(synth.hidden_states(Bn, S, hd, seed=0)).to(dev)
 ws = torch.empty(L.workspace_size(T), dtype=torch.uint8, device=dev)
-calls, _ = bench.stage_calls(M, L, h_in, ws, T, torch.cuda.current_stream())
+calls, _ = bench.stage_calls(M, L, h_in, Bn, T, torch.cuda.current_stream())
 for c in calls:
     c[1]()
 name = os.environ.get("STAGE", "gemm_ffn1")
