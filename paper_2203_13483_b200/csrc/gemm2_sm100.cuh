@@ -59,7 +59,7 @@ struct Epi2Params {
     Ln2Params ln;        // kLn only
 };
 
-template <int BN_, int EPI_ = 8, int UNP_ = 8, bool LUT4_ = false, bool LN_ = false>
+template <int BN_, int EPI_ = 8, int UNP_ = 8, bool LUT4_ = false, bool LN_ = false, int LNB_ = 2>
 struct Gemm2Cfg {
     static constexpr bool kLn = LN_;                 // fused residual + LayerNorm epilogue
     static constexpr bool kRegSplit = LUT4_ || LN_;  // setmaxnreg per role
@@ -74,8 +74,11 @@ struct Gemm2Cfg {
     static constexpr int kAP = BM * BK / 2;
     static constexpr int kBP = BNH * BK / 2;
     static constexpr int kStageP = kAP + kBP;
-    static constexpr int S8 = LN_ ? 3 : 4;            // kLn: smem goes to the epilogue's TMA staging
-    static constexpr int SP = LN_ ? 2 : 3;
+    // kLn: LNB_ residual/output boxes per epilogue warp; two boxes (short K,
+    // epilogue-bound) take smem from the rings, one box (long K) keeps them
+    static constexpr int kBoxes = LNB_;
+    static constexpr int S8 = LN_ && LNB_ > 1 ? 3 : 4;
+    static constexpr int SP = LN_ && LNB_ > 1 ? 2 : 3;
     static constexpr int kEpiWarps = EPI_;          // 8 or 16 (2 or 4 per TMEM lane quadrant)
     static constexpr int kUnpWarps = UNP_;          // 8 or 4
     static constexpr int kThreads = 32 * (4 + kEpiWarps + kUnpWarps);
@@ -92,7 +95,7 @@ struct Gemm2Cfg {
     static constexpr int kStgBufs = kLut4 && EPI_ <= 8 ? 2 : 1;
     // kLn: two 32 x 32 fp32 SWIZZLE_128B blocks (residual in / LN output out)
     // and two 32-row code blocks (<= 32 B per row) per warp
-    static constexpr int kStagePerWarp = kLn ? 2 * 4096 + 2 * 1024 : (kLut4 ? 512 * kStgBufs : 2048);
+    static constexpr int kStagePerWarp = kLn ? LNB_ * (4096 + 1024) : (kLut4 ? 512 * kStgBufs : 2048);
     static constexpr int kStaging = kEpiWarps * kStagePerWarp;
     static constexpr int kTabBytes = kLn ? 0 : (kLut4 ? (int)rq::kSmem4Bytes : (int)rq::kSmemBytes);
     // kLut4 register split (setmaxnreg; must fit the launch allocation)
@@ -486,7 +489,7 @@ __device__ __forceinline__ void ln_epilogue(const Epi2Params& p, const LnMaps& l
     uint8_t* stg = staging + e * Cfg::kStagePerWarp;       // [2] x 4 KB boxes, [2] x 1 KB code blocks
     const uint32_t stg_s = ptx::smem_u32(stg);
     uint64_t* rb = rbars + 2 * e;
-    uint32_t rph[2] = {0u, 0u};
+    uint32_t rph[2] = {0u, 0u};   // per box (NB <= 2)
     // lane l's 16-byte chunk c4 of its row in a SWIZZLE_128B 32 x 128 B box
     auto sw = [lane](int c4) { return (uint32_t)(lane * 128 + ((c4 ^ (lane & 7)) << 4)); };
     uint64_t* stats_g = reinterpret_cast<uint64_t*>(L.stats) + (size_t)group * (2 * np * 2 * BM);
@@ -499,10 +502,11 @@ __device__ __forceinline__ void ln_epilogue(const Epi2Params& p, const LnMaps& l
 #ifdef MKQ_GTRACE
     int gt_n = 0;
 #endif
-    auto load_res = [&](int tl, int ch) {   // TMA: residual box (tile tl, chunk ch) into buffer ch & 1
+    constexpr int NB = Cfg::kBoxes;
+    auto load_res = [&](int tl, int ch) {   // TMA: residual box (tile tl, chunk ch) into box ch % NB
         if (lane == 0 && tl < t_end) {
-            ptx::mbar_arrive_expect_tx(&rb[ch & 1], 4096);
-            ptx::tma_load_2d(&lm.r, &rb[ch & 1], stg + (ch & 1) * 4096, ncol0 + c0 + 32 * ch,
+            ptx::mbar_arrive_expect_tx(&rb[ch % NB], 4096);
+            ptx::tma_load_2d(&lm.r, &rb[ch % NB], stg + (ch % NB) * 4096, ncol0 + c0 + 32 * ch,
                              tl * 2 * BM + rank * BM + q * 32);
         }
     };
@@ -515,8 +519,8 @@ __device__ __forceinline__ void ln_epilogue(const Epi2Params& p, const LnMaps& l
         // both boxes must have been read by the previous tile's output stores
         if (lane == 0) ptx::tma_store_wait_read<0>();
         __syncwarp();
-        load_res(tile, 0);
-        load_res(tile, 1);
+#pragma unroll
+        for (int b = 0; b < NB; ++b) load_res(tile, b);
         ptx::mbar_wait_sleep<64>(&tfull[ab], aph);
         GTRACE(42);
         ptx::tc_fence_after();
@@ -527,12 +531,12 @@ __device__ __forceinline__ void ln_epilogue(const Epi2Params& p, const LnMaps& l
             ptx::tmem_ld_32x32b_x32(tmem_base + lane_off + ab * BN + c0 + 32 * ch, v);
             ptx::tmem_ld_wait_regs(v);
             GTRACE(52);
-            ptx::mbar_wait(&rb[ch & 1], rph[ch & 1]);
-            rph[ch & 1] ^= 1u;
+            ptx::mbar_wait(&rb[ch % NB], rph[ch % NB]);
+            rph[ch % NB] ^= 1u;
             GTRACE(53);
 #pragma unroll
             for (int c4 = 0; c4 < 8; ++c4) {
-                const float4 rs = lds128f(stg_s + (ch & 1) * 4096 + sw(c4));
+                const float4 rs = lds128f(stg_s + (ch % NB) * 4096 + sw(c4));
 #pragma unroll
                 for (int t = 0; t < 4; t += 2) {
                     const int i = 4 * c4 + t;
@@ -546,10 +550,10 @@ __device__ __forceinline__ void ln_epilogue(const Epi2Params& p, const LnMaps& l
                     r[32 * ch + i + 1] = rr.y;
                 }
             }
-            if (ch + 2 < kCh) {   // this box is consumed: refill it with chunk ch + 2
+            if (ch + NB < kCh) {   // this box is consumed: refill it with chunk ch + NB
                 ptx::fence_proxy_async_smem();
                 __syncwarp();
-                load_res(tile, ch + 2);
+                load_res(tile, ch + NB);
             }
         }
         // the accumulator buffer is free for the MMA of tile it+2
@@ -633,10 +637,10 @@ __device__ __forceinline__ void ln_epilogue(const Epi2Params& p, const LnMaps& l
         // output: LN(r) staged per 32-column chunk in the swizzled boxes, TMA-stored
 #pragma unroll
         for (int ch = 0; ch < kCh; ++ch) {
-            uint8_t* box = stg + (ch & 1) * 4096;
-            uint8_t* cbx = stg + 2 * 4096 + (ch & 1) * 1024;
+            uint8_t* box = stg + (ch % NB) * 4096;
+            uint8_t* cbx = stg + NB * 4096 + (ch % NB) * 1024;
             GTRACE(50);
-            if (lane == 0) ptx::tma_store_wait_read<1>();   // the stores of chunk ch - 2 have read these
+            if (lane == 0) ptx::tma_store_wait_read<NB - 1>();   // the stores of chunk ch - NB have read these
             __syncwarp();
             float o[32];
 #pragma unroll

@@ -285,15 +285,17 @@ mkq_status launch_gemm2(const void* a, int64_t lda, const void* w, int64_t ldw, 
 // Fused W4A4 GEMM + residual + LayerNorm (kLn; Gemm2Cfg<256, 8, 4, false, true>):
 // one persistent CTA pair per TPC, pairs grouped np at a time; row statistics
 // exchanged through `ws` (counters zeroed here, before the launch).
-using LnCfg = mkq::Gemm2Cfg<256, 8, 4, false, true>;
+using LnCfg = mkq::Gemm2Cfg<256, 8, 4, false, true, 2>;      // short K (epilogue-bound): 2 boxes per warp
+using LnCfgK = mkq::Gemm2Cfg<256, 8, 4, false, true, 1>;     // long K (mainloop-bound): deeper rings
 int ln_groups(int sms, int np) { return (sms / 2) / np; }
 size_t ln_ws_bytes(int sms, int np) {
     const int groups = ln_groups(sms, np);
     return (size_t)groups * 2 * np * 256 * sizeof(uint64_t);
 }
 
-mkq_status launch_gemm2_ln(const void* a, int64_t lda, const void* w, int64_t ldw, int M, int N, int K,
-                           mkq::Epi2Params& ep, void* ws, int sms, cudaStream_t st) {
+template <class LnCfg>
+mkq_status launch_gemm2_ln_cfg(const void* a, int64_t lda, const void* w, int64_t ldw, int M, int N, int K,
+                               mkq::Epi2Params& ep, void* ws, int sms, cudaStream_t st) {
     static bool attr_set[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -338,6 +340,14 @@ mkq_status launch_gemm2_ln(const void* a, int64_t lda, const void* w, int64_t ld
                  ma, mb, ep, M, N, K, lm);
     if (e != cudaSuccess) return cuda_fail(e, "gemm_ln launch");
     return MKQ_OK;
+}
+
+mkq_status launch_gemm2_ln(const void* a, int64_t lda, const void* w, int64_t ldw, int M, int N, int K,
+                           mkq::Epi2Params& ep, void* ws, int sms, cudaStream_t st) {
+    static const int boxes = [] { const char* v = getenv("MKQ_LN_BOXES"); return v ? atoi(v) : 0; }();   // diagnostics
+    const bool long_k = boxes ? boxes == 1 : K >= 2048;
+    return long_k ? launch_gemm2_ln_cfg<LnCfgK>(a, lda, w, ldw, M, N, K, ep, ws, sms, st)
+                  : launch_gemm2_ln_cfg<LnCfg>(a, lda, w, ldw, M, N, K, ep, ws, sms, st);
 }
 
 // Small-M plan (the paper's Table 2 regime of a few
