@@ -77,8 +77,9 @@ struct Gemm2Cfg {
     // kLn: LNB_ residual/output boxes per epilogue warp; two boxes (short K,
     // epilogue-bound) take smem from the rings, one box (long K) keeps them
     static constexpr int kBoxes = LNB_;
-    static constexpr int S8 = LN_ && LNB_ > 1 ? 3 : 4;
-    static constexpr int SP = LN_ && LNB_ > 1 ? 2 : 3;
+    static constexpr bool kSmallRing = LN_ && LNB_ * (4096 + 1024) * EPI_ > 48 * 1024;
+    static constexpr int S8 = kSmallRing ? 3 : 4;
+    static constexpr int SP = kSmallRing ? 2 : 3;
     static constexpr int kEpiWarps = EPI_;          // 8 or 16 (2 or 4 per TMEM lane quadrant)
     static constexpr int kUnpWarps = UNP_;          // 8 or 4
     static constexpr int kThreads = 32 * (4 + kEpiWarps + kUnpWarps);
@@ -527,15 +528,18 @@ __device__ __forceinline__ void ln_epilogue(const Epi2Params& p, const LnMaps& l
         float r[kCW];
 #pragma unroll
         for (int ch = 0; ch < kCh; ++ch) {
-            uint32_t v[32];
-            ptx::tmem_ld_32x32b_x32(tmem_base + lane_off + ab * BN + c0 + 32 * ch, v);
-            ptx::tmem_ld_wait_regs(v);
             GTRACE(52);
             ptx::mbar_wait(&rb[ch % NB], rph[ch % NB]);
             rph[ch % NB] ^= 1u;
             GTRACE(53);
 #pragma unroll
-            for (int c4 = 0; c4 < 8; ++c4) {
+            for (int hv = 0; hv < 2; ++hv) {   // 16 accumulator columns at a time (register budget)
+            uint32_t v16[16];
+            ptx::tmem_ld_32x32b_x16(tmem_base + lane_off + ab * BN + c0 + 32 * ch + 16 * hv, v16);
+            ptx::tmem_ld_wait();
+            const uint32_t* v = v16 - 16 * hv;   // v[i] for i in [16 hv, 16 hv + 16)
+#pragma unroll
+            for (int c4 = 4 * hv; c4 < 4 * hv + 4; ++c4) {
                 const float4 rs = lds128f(stg_s + (ch % NB) * 4096 + sw(c4));
 #pragma unroll
                 for (int t = 0; t < 4; t += 2) {
@@ -549,6 +553,7 @@ __device__ __forceinline__ void ln_epilogue(const Epi2Params& p, const LnMaps& l
                     r[32 * ch + i] = rr.x;
                     r[32 * ch + i + 1] = rr.y;
                 }
+            }
             }
             if (ch + NB < kCh) {   // this box is consumed: refill it with chunk ch + NB
                 ptx::fence_proxy_async_smem();

@@ -287,6 +287,7 @@ mkq_status launch_gemm2(const void* a, int64_t lda, const void* w, int64_t ldw, 
 // exchanged through `ws` (counters zeroed here, before the launch).
 using LnCfg = mkq::Gemm2Cfg<256, 8, 4, false, true, 2>;      // short K (epilogue-bound): 2 boxes per warp
 using LnCfgK = mkq::Gemm2Cfg<256, 8, 4, false, true, 1>;     // long K (mainloop-bound): deeper rings
+using LnCfg16 = mkq::Gemm2Cfg<256, 16, 4, false, true, 1>;   // short K, 16 epilogue warps (diagnostics)
 int ln_groups(int sms, int np) { return (sms / 2) / np; }
 size_t ln_ws_bytes(int sms, int np) {
     const int groups = ln_groups(sms, np);
@@ -345,6 +346,7 @@ mkq_status launch_gemm2_ln_cfg(const void* a, int64_t lda, const void* w, int64_
 mkq_status launch_gemm2_ln(const void* a, int64_t lda, const void* w, int64_t ldw, int M, int N, int K,
                            mkq::Epi2Params& ep, void* ws, int sms, cudaStream_t st) {
     static const int boxes = [] { const char* v = getenv("MKQ_LN_BOXES"); return v ? atoi(v) : 0; }();   // diagnostics
+    if (boxes == 16) return launch_gemm2_ln_cfg<LnCfg16>(a, lda, w, ldw, M, N, K, ep, ws, sms, st);
     const bool long_k = boxes ? boxes == 1 : K >= 2048;
     return long_k ? launch_gemm2_ln_cfg<LnCfgK>(a, lda, w, ldw, M, N, K, ep, ws, sms, st)
                   : launch_gemm2_ln_cfg<LnCfg>(a, lda, w, ldw, M, N, K, ep, ws, sms, st);
