@@ -194,14 +194,19 @@ __device__ __forceinline__ uint32_t pack_byte4(int a, int b, int c, int d) {
            ((uint32_t)(d & 0xFF) << 24);
 }
 
+// R11: round-to-nearest-even of each fp32 value, a in the low half: one
+// cvt.rn.*x2.f32 (F2FP.PACK_AB) per pair instead of two scalar conversions
+// through the MIO pipe (the QKV epilogue's top stall in the r02 profile)
 __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
-    __nv_bfloat16 x = __float2bfloat16_rn(a), y = __float2bfloat16_rn(b);
-    return (uint32_t)__bfloat16_as_ushort(x) | ((uint32_t)__bfloat16_as_ushort(y) << 16);
+    uint32_t r;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
+    return r;
 }
 
 __device__ __forceinline__ uint32_t pack_f16x2(float a, float b) {
-    __half x = __float2half_rn(a), y = __float2half_rn(b);
-    return (uint32_t)__half_as_ushort(x) | ((uint32_t)__half_as_ushort(y) << 16);
+    uint32_t r;
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
+    return r;
 }
 
 }  // namespace mkq

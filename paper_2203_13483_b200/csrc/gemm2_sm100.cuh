@@ -85,11 +85,10 @@ struct Gemm2Cfg {
     static constexpr int kThreads = 32 * (4 + kEpiWarps + kUnpWarps);
     static constexpr uint32_t kTmemCols = 2 * BN;
     static constexpr int kColsPerWarp = BN / (kEpiWarps / 4);
-    // (sc, b) per column: 2 tile buffers x BN (shared by the epilogue), or
-    // (kLut4) one private kColsPerWarp slice per epilogue warp, or (kLn)
+    // (sc, b) per column: one private kColsPerWarp slice per epilogue warp
+    // (loaded one tile ahead; no epilogue-wide barrier per tile), or (kLn)
     // (sc, b, gamma, beta) of the BN fixed columns + the quadrant partial sums
-    static constexpr int kScb = kLn ? BN * 16 + (kEpiWarps / 4) * BM * 8
-                                    : (kLut4 ? kEpiWarps * kColsPerWarp * 8 : 2 * BN * 8);
+    static constexpr int kScb = kLn ? BN * 16 + (kEpiWarps / 4) * BM * 8 : kEpiWarps * kColsPerWarp * 8;
     // per epilogue warp: kLut4 one or (8 warps) two 32 x 16 B int4 blocks
     // (double-buffered TMA stores), else one 32 x 64 B output block; kLn
     // stores from registers
@@ -896,7 +895,7 @@ __device__ __forceinline__ void gemm2_body(const CUtensorMap& tmA, const CUtenso
                 v2[c] = make_float2(sw, bn);
             }
         };
-        if constexpr (Cfg::kLut4) load_scales(t_begin);
+        load_scales(t_begin);
         // this lane's replica of the compact table, and the same minus the cell
         // bias (bits(2^23) * 128 = 2^31 mod 2^32), held in vector registers
         const uint32_t tab = ptx::smem_u32(th) + 4u * (uint32_t)lane;
@@ -908,7 +907,6 @@ __device__ __forceinline__ void gemm2_body(const CUtensorMap& tmA, const CUtenso
             const int n0 = tn0(tile);
             const int ab = it & 1;
             const uint32_t aph = (it >> 1) & 1;
-            float2* sb = scb + ab * BN;
             if constexpr (Cfg::kLut4) {
                 // per-warp (sc, b) of this warp's kColsPerWarp columns: no epilogue-wide
                 // barrier per tile, warps slip freely against each other
@@ -1011,21 +1009,24 @@ __device__ __forceinline__ void gemm2_body(const CUtensorMap& tmA, const CUtenso
                 GTRACE(8);
                 continue;
             }
-            bool tiny = false;
-            float sc = 1.0f, bn = 0.0f;
-            {   // per-column scale and bias of this tile
-                const int n = n0 + et;
-                if (et < BN && n < N) {
-                    sc = __fmul_rn(ep.s_a, __ldg(ep.s_w + n));
-                    bn = ep.bias ? __ldg(ep.bias + n) : 0.0f;
-                    tiny = !(sc >= 0x1p-118f);   // sc * 2^-8 would not be normal (or sc is not > 0)
-                }
+            // per-warp (sc, b) of this warp's kColsPerWarp columns (loaded one tile
+            // ahead), written as one float2 per column; the 2^-8 fold is decided per
+            // warp (folded and unfolded dequant give identical bits, R4)
+            float2* wsb = scb + e * Cfg::kColsPerWarp;
+            bool ok = true;
+#pragma unroll
+            for (int c = 0; c < kCW; ++c) {
+                v2[c].x = __fmul_rn(ep.s_a, v2[c].x);   // sc = fl(s_a * s_w[n]) (R4); 1.0 * s_a past N
+                ok = ok && v2[c].x >= 0x1p-118f;
             }
-            // fold the >> 8 into sc unless some column's sc is too small (rare; tile-uniform)
-            const bool fold = !ptx::named_bar_sync_or(1, kEpiThreads, tiny);
-            if (et < BN) sb[et] = make_float2(fold ? __fmul_rn(sc, 0x1p-8f) : sc, bn);
-            ptx::named_bar_sync(1, kEpiThreads);
-            MKQ_WAIT_SLEEP(128, &tfull[ab], aph);
+            const bool fold = __all_sync(0xffffffffu, ok);
+            __syncwarp();
+#pragma unroll
+            for (int c = 0; c < kCW; ++c)
+                wsb[32 * c + lane] = make_float2(fold ? __fmul_rn(v2[c].x, 0x1p-8f) : v2[c].x, v2[c].y);
+            __syncwarp();
+            load_scales(tile + t_step);   // in flight during this tile
+            ptx::mbar_wait_sleep<64>(&tfull[ab], aph);
             ptx::tc_fence_after();
             const int row0 = m0 + q * 32;
             {
@@ -1045,15 +1046,18 @@ __device__ __forceinline__ void gemm2_body(const CUtensorMap& tmA, const CUtenso
                     uint32_t v[16];
                     ptx::tmem_ld_32x32b_x16(tmem_base + ((uint32_t)(q * 32) << 16) + ab * BN + cl + 16 * h2, v);
                     ptx::tmem_ld_wait();
-                    epi2_half(ep, L, use_table, fold, ptx::smem_u32(sb + cl + 16 * h2), v, stage, lane, h2);
+                    epi2_half(ep, L, use_table, fold, ptx::smem_u32(wsb + (cl - h * Cfg::kColsPerWarp) + 16 * h2), v,
+                              stage, lane, h2);
                     if (h2 == 1 || wide) {
                         ptx::fence_proxy_async_smem();
                         __syncwarp();
+#ifndef MKQ_ABL_NOSTORE2   // ablation (diagnostics only): no output store
                         if (lane == 0) {
                             const int nn = n + (wide ? 16 * h2 : 0);
                             ptx::tma_store_2d(&tmO, stage, ep.mode == OUT_I4 ? nn / 2 : nn, row0);
                             ptx::tma_store_commit();
                         }
+#endif
                     }
                 }
             }
