@@ -421,7 +421,10 @@ def run_ours(args):
     h_pin = torch.from_numpy(h_host).pin_memory()
     o_pin = torch.empty(h_host.shape, dtype=torch.float32).pin_memory()
     e2e_steps = max(2, min(args.steps, 5))
-    nch = 8 if B % 8 == 0 and B >= 16 else 1
+    # chunks of whole sequences: more chunks shorten the un-overlapped first H2D /
+    # last D2H (PCIe-bound; env MKQ_E2E_CHUNKS overrides, diagnostics)
+    # (8: 12.49 ms, 16: 12.23, 32: 12.66 at C4: 2 x 537 MB at ~44 GB/s per PCIe direction)
+    nch = int(os.environ.get("MKQ_E2E_CHUNKS", "0")) or next((c for c in (16, 8, 4, 2) if B % c == 0), 1)
     Bc, Tc = B // nch, (B // nch) * S
     ws_c = torch.empty(L.workspace_size(Tc), dtype=torch.uint8, device=dev)
     s_in, s_out = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
