@@ -610,6 +610,32 @@ def column_parallel_ffn(torch, L, dev, world, rank, barrier, max_ranks, stream, 
         once(True)
     ms = {n: max_ranks(float(np.mean(v))) for n, v in times.items()}
     tot = max_ranks(float(np.sum([np.mean(v) for v in times.values()])))
+    fused = None
+    if os.environ.get("MKQ_BENCH_FUSED_AG") == "1":
+        # NEXT(4): FFN1 with the all-gather fused into its epilogue (peer TMA
+        # stores through CUDA IPC + arrival counters), then the same FFN2 path
+        ref_out = once(False)
+        cp.setup_fused_gather(T)
+        barrier()
+        out = cp.forward_fused(codes, h1, stream=stream)
+        torch.cuda.synchronize(dev)
+        same = bool(torch.equal(out, ref_out))
+        ft = []
+        for _ in range(reps):
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(stream):
+                e0.record(stream)
+                cp.forward_fused(codes, h1, stream=stream)
+                e1.record(stream)
+            torch.cuda.synchronize(dev)
+            ft.append(e0.elapsed_time(e1))
+        barrier()
+        cp.close_fused_gather()
+        same_all = max_ranks(0.0 if same else 1.0) == 0.0
+        fused = {"ms_total": round(max_ranks(float(np.mean(ft))), 4), "bit_identical_to_nccl_path": same_all,
+                 "collective": "FFN1 epilogue TMA stores into every rank's buffer (CUDA IPC) + counters; "
+                               "NCCL all_gather for the fp32 FFN2 output"}
     g1 = T * F / 2          # bytes of the gathered int4 FFN2 input
     g2 = T * hd * 4         # bytes of the gathered fp32 FFN2 output
     busbw = lambda nbytes, t: nbytes / (t * 1e-3) / 1e9 * (world - 1) / world  # noqa: E731
@@ -622,7 +648,8 @@ def column_parallel_ffn(torch, L, dev, world, rank, barrier, max_ranks, stream, 
             "stages_ms": {k: round(v, 4) for k, v in ms.items()},
             "allgather_int4": {"bytes": int(g1), "busbw_gbs": round(busbw(g1, ms["allgather_int4"]), 1)},
             "allgather_f32": {"bytes": int(g2), "busbw_gbs": round(busbw(g2, ms["allgather_f32"]), 1)},
-            "nvlink_ref_gbs": 770.0, "collective": "NCCL all_gather_into_tensor (torch.distributed)"}
+            "nvlink_ref_gbs": 770.0, "collective": "NCCL all_gather_into_tensor (torch.distributed)",
+            "fused_allgather": fused}
 
 
 def small_configs(torch, dev, pk, regime):

@@ -188,6 +188,37 @@ MKQ_API mkq_status mkq_gemm_residual_ln(const void *a, int64_t lda_bytes, const 
                                         float s_q, int qmin, int qmax, void *q, int64_t ldq, void *ws,
                                         size_t ws_bytes, void *stream);
 
+/* NEXT(4) fused communication for the column-parallel FFN:
+ * the FFN1 GEMM of one rank (W4A4, GELU + int4 requantize through the compact
+ * table, epi->out = MKQ_OUT_I4 with epi->requant_table) stores every output
+ * tile directly into the gathered FFN2-input buffer of every rank at column
+ * col0 (this rank's block), instead of a local output + NCCL all-gather:
+ *   outs[g]     [device, valid in this process: the local buffer or a peer's
+ *               CUDA-IPC mapping] packed int4 [M, >= col0 + N], row stride
+ *               ldo bytes (16-byte multiple);
+ *   counters[g] [device, same] uint32: after all its stores are complete each
+ *               CTA adds 1 to every counters[g] (release, system scope); a
+ *               launch adds mkq_gemm_gather_arrivals(M, N) per counter.
+ * N % 256 == 0, K <= 1024 (the FFN1 shape).  The consumer blocks its stream
+ * with mkq_wait_counter(own counter, target) before reading its buffer.
+ * Reusing a gathered buffer needs the peers' readers to be done with it
+ * (the caller's barrier).  Codes are bit-identical to mkq_gemm_w4a4. */
+MKQ_API int mkq_gemm_gather_arrivals(int64_t M, int64_t N);
+MKQ_API mkq_status mkq_gemm_w4a4_gather(const void *a, int64_t lda_bytes, const void *w, int64_t ldw_bytes,
+                                        int64_t M, int64_t N, int64_t K, float s_a, const float *s_w,
+                                        const float *bias, const mkq_epilogue *epi, void *const *outs, int nout,
+                                        int64_t col0, int64_t ldo_bytes, uint32_t *const *counters, void *stream);
+/* Block `stream` until *counter >= target (acquire, system scope). */
+MKQ_API mkq_status mkq_wait_counter(const uint32_t *counter, uint32_t target, void *stream);
+/* CUDA IPC plumbing for the peer buffers.  get_handle writes the 64-byte
+ * handle of the allocation containing dev_ptr and dev_ptr's byte offset in
+ * it; a peer maps the allocation with open_handle (-> *base; the buffer is
+ * base + offset) and unmaps it with close(base).  Errors: MKQ_ERR_NULL,
+ * MKQ_ERR_CUDA (message in mkq_last_error()). */
+MKQ_API mkq_status mkq_ipc_get_handle(const void *dev_ptr, void *handle64, int64_t *offset);
+MKQ_API mkq_status mkq_ipc_open_handle(const void *handle64, void **base);
+MKQ_API mkq_status mkq_ipc_close(void *base);
+
 /* Diagnostics / tests: GEMM tile plan for small M.  -1 = heuristic (default;
  * also the MKQ_SMALL_M environment variable), 0 = never the small-M plan,
  * 1 = always the tcgen05 cluster split-K plan, 2 = always the mma.sync

@@ -33,6 +33,12 @@ SIGNATURES = {
     "mkq_gemm_residual_ln_workspace_size": (SZ, [I64, I64]),
     "mkq_gemm_residual_ln": (I32, [P, I64, P, I64, I64, I64, I64, F32, P, P, P, I64, P, P, F32, P, I64, I32, F32,
                                    I32, I32, P, I64, P, SZ, P]),
+    "mkq_gemm_gather_arrivals": (I32, [I64, I64]),
+    "mkq_gemm_w4a4_gather": (I32, [P, I64, P, I64, I64, I64, I64, F32, P, P, P, P, I32, I64, I64, P, P]),
+    "mkq_wait_counter": (I32, [P, ctypes.c_uint32, P]),
+    "mkq_ipc_get_handle": (I32, [P, P, P]),
+    "mkq_ipc_open_handle": (I32, [P, P]),
+    "mkq_ipc_close": (I32, [P]),
     "mkq_set_small_m_mode": (None, [I32]),
     "mkq_requant_table_size": (SZ, []),
     "mkq_requant_table": (I32, [I32, F32, I32, I32, P, SZ, P]),

@@ -421,6 +421,18 @@ __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
     return v;
 }
 
+// Fused all-gather (NEXT(4), column-parallel FFN): the compact-table int4
+// epilogue stores every output tile into `n` gathered buffers (this rank's
+// and its peers', mapped into this process) at column `col0` + n, then each
+// CTA signals every buffer owner's counter once (system-scope release) after
+// its stores are complete.
+constexpr int kMaxGather = 8;
+struct GatherMaps {
+    CUtensorMap m[kMaxGather];
+    uint32_t* counters[kMaxGather];
+    int n, col0;
+};
+
 // Tensor maps of the kLn epilogue: residual and LN output fp32 [M, N] in
 // 32 x 32 SWIZZLE_128B boxes, the codes [M, N*qbits/8] in 32-row boxes of
 // 16 (int4) or 32 (int8) bytes.
@@ -700,7 +712,8 @@ __device__ __forceinline__ void ln_epilogue(const Epi2Params& p, const LnMaps& l
 // gemm_w4a4_ln_kernel (kLn); `lm` is dereferenced only by the kLn epilogue.
 template <class Cfg>
 __device__ __forceinline__ void gemm2_body(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmO,
-                                           const Epi2Params& p, int M, int N, int K, const LnMaps* lmp) {
+                                           const Epi2Params& p, int M, int N, int K, const LnMaps* lmp,
+                                           const GatherMaps* gm = nullptr) {
     constexpr int BM = Cfg::BM, BN = Cfg::BN, BNH = Cfg::BNH, S8 = Cfg::S8, SP = Cfg::SP;
     constexpr int kEpiThreads = 32 * Cfg::kEpiWarps;
     constexpr int kUnpThreads = 32 * Cfg::kUnpWarps;
@@ -986,7 +999,11 @@ __device__ __forceinline__ void gemm2_body(const CUtensorMap& tmA, const CUtenso
                     __syncwarp();
 #ifndef MKQ_ABL_L4NOSTORE
                     if (lane == 0 && n < N) {
-                        ptx::tma_store_2d(&tmO, stg, n / 2, row0);
+                        if (gm) {   // fused all-gather: the tile into every rank's gathered buffer
+                            for (int g = 0; g < gm->n; ++g) ptx::tma_store_2d(&gm->m[g], stg, (gm->col0 + n) / 2, row0);
+                        } else {
+                            ptx::tma_store_2d(&tmO, stg, n / 2, row0);
+                        }
                         ptx::tma_store_commit();
                     }
 #endif
@@ -1067,6 +1084,19 @@ __device__ __forceinline__ void gemm2_body(const CUtensorMap& tmA, const CUtenso
             if (lane == 0) ptx::mbar_arrive_remote(ptx::mapa(&tempty[ab], 0));
         }
         if (lane == 0) ptx::tma_store_wait<0>();
+        if (gm) {
+            // this warp's stores are complete; make them visible beyond the GPU, then
+            // one release increment per CTA on every gathered buffer's owner counter
+            if (lane == 0) {
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                __threadfence_system();
+            }
+            __syncwarp();
+            ptx::named_bar_sync(1, kEpiThreads);
+            if (threadIdx.x == 128)
+                for (int g = 0; g < gm->n; ++g)
+                    asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(gm->counters[g]) : "memory");
+        }
         }
     } else {
         if constexpr (Cfg::kRegSplit) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(Cfg::kRegUnp));
@@ -1156,6 +1186,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
                         const Epi2Params p, int M, int N, int K, const __grid_constant__ LnMaps lm) {
     static_assert(Cfg::kLn, "plain epilogues: gemm_w4a4_2cta_kernel");
     gemm2_body<Cfg>(tmA, tmB, tmA, p, M, N, K, &lm);
+}
+
+template <class Cfg>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg::kThreads, 1)
+    gemm_w4a4_gather_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                            const Epi2Params p, int M, int N, int K, const __grid_constant__ GatherMaps gm) {
+    static_assert(Cfg::kLut4, "the fused all-gather is the compact-table int4 epilogue");
+    gemm2_body<Cfg>(tmA, tmB, gm.m[0], p, M, N, K, nullptr, &gm);
+}
+
+// Consumer side of the fused all-gather: block the stream until `counter`
+// (this rank's, incremented by the producers' CTAs) reaches `target`.
+__global__ void wait_counter_kernel(const uint32_t* counter, uint32_t target) {
+    uint32_t v;
+    do {
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
+        if (v < target) __nanosleep(256);
+    } while (v < target);
 }
 
 }  // namespace mkq

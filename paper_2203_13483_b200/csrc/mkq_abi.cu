@@ -673,6 +673,121 @@ mkq_status mkq_gemm_w8a8(const void* a, int64_t lda, const void* w, int64_t ldw,
 
 void mkq_set_small_m_mode(int mode) { g_small_mode.store(mode < 0 ? -1 : (mode > 2 ? 2 : mode)); }
 
+// ------------------------------------------------------------------ NEXT(4) fused all-gather
+using GatherCfg = mkq::Gemm2Cfg<256, 16, 4, true>;
+
+static int gather_grid(int64_t M, int64_t N, int sms) {
+    const int64_t tiles = ((M + 2 * GatherCfg::BM - 1) / (2 * GatherCfg::BM)) * ((N + GatherCfg::BN - 1) / GatherCfg::BN);
+    const int clusters = (int)(tiles < sms / 2 ? tiles : sms / 2);
+    return 2 * clusters;
+}
+
+int mkq_gemm_gather_arrivals(int64_t M, int64_t N) {
+    int sms = 148;
+    if (check_device(&sms) != MKQ_OK) sms = 148;
+    return M > 0 && N > 0 ? gather_grid(M, N, sms) : 0;
+}
+
+mkq_status mkq_gemm_w4a4_gather(const void* a, int64_t lda, const void* w, int64_t ldw, int64_t M, int64_t N,
+                                int64_t K, float s_a, const float* s_w, const float* bias, const mkq_epilogue* epi,
+                                void* const* outs, int nout, int64_t col0, int64_t ldo, uint32_t* const* counters,
+                                void* stream) {
+    if (M < 0 || N < 0 || K < 0) return fail(MKQ_ERR_SHAPE, "negative dimension");
+    if (M == 0) return MKQ_OK;
+    if (!a || !w || !s_w || !epi || !outs || !counters) return fail(MKQ_ERR_NULL, "a, w, s_w, epi, outs, counters");
+    if (nout < 1 || nout > mkq::kMaxGather) return fail(MKQ_ERR_RANGE, "nout must be in [1, %d]", mkq::kMaxGather);
+    if (epi->out != MKQ_OUT_I4 || !epi->requant_table) return fail(MKQ_ERR_RANGE, "the fused all-gather is the int4 requant (table) epilogue");
+    if (!code_range_ok(4, epi->qmin_out, epi->qmax_out)) return fail(MKQ_ERR_RANGE, "qmin/qmax");
+    if (!finite_pos(epi->s_out) || !finite_pos(s_a)) return fail(MKQ_ERR_SCALE, "s_a and s_out must be > 0 and finite");
+    if (N % 256 || K % 32 || K > 1024 || K < 32) return fail(MKQ_ERR_SHAPE, "N % 256 == 0 and K in [32, 1024], K % 32 == 0");
+    if (col0 < 0 || col0 % 32 || ldo < (col0 + N) / 2 || ldo % 16) return fail(MKQ_ERR_SHAPE, "col0 / ldo");
+    if (lda < K / 2 || ldw < K / 2 || lda % 16 || ldw % 16 || !aligned16(a) || !aligned16(w) || !aligned16(epi->requant_table))
+        return fail(MKQ_ERR_ALIGN, "operands");
+    for (int g = 0; g < nout; ++g) {
+        if (!outs[g] || !counters[g]) return fail(MKQ_ERR_NULL, "outs[%d] / counters[%d]", g, g);
+        if (!aligned16(outs[g]) || (reinterpret_cast<uintptr_t>(counters[g]) & 3)) return fail(MKQ_ERR_ALIGN, "outs / counters");
+    }
+    int sms = 0;
+    mkq_status st = check_device(&sms);
+    if (st != MKQ_OK) return st;
+    static bool attr_set[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!attr_set[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(mkq::gemm_w4a4_gather_kernel<GatherCfg>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, GatherCfg::kSmem);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+        attr_set[dev] = true;
+    }
+    mkq::EpiParams ep{MKQ_OUT_I4, epi->gelu, s_a, s_w, bias, epi->s_out, epi->qmin_out, epi->qmax_out, outs[0], ldo};
+    mkq::Epi2Params p2{ep, epi->requant_table, {}};
+    CUtensorMap ma, mb;
+    st = make_map(&ma, a, (uint64_t)K / 2, (uint64_t)M, (uint64_t)lda, GatherCfg::BK / 2, GatherCfg::BM, false);
+    if (st != MKQ_OK) return st;
+    st = make_map(&mb, w, (uint64_t)K / 2, (uint64_t)N, (uint64_t)ldw, GatherCfg::BK / 2, GatherCfg::BNH, false);
+    if (st != MKQ_OK) return st;
+    mkq::GatherMaps gm{};
+    for (int g = 0; g < nout; ++g) {
+        // the gathered buffer is [M, >= col0 + N] codes; its row stride ldo bytes
+        st = make_out_map(&gm.m[g], outs[g], MKQ_OUT_I4, M, 2 * ldo, ldo);
+        if (st != MKQ_OK) return st;
+        gm.counters[g] = counters[g];
+    }
+    gm.n = nout;
+    gm.col0 = (int)col0;
+    PdlScope pdl_scope(M);
+    cudaError_t e = launch_k(mkq::gemm_w4a4_gather_kernel<GatherCfg>, dim3(gather_grid(M, N, sms)),
+                             dim3(GatherCfg::kThreads), GatherCfg::kSmem, static_cast<cudaStream_t>(stream), 1, ma, mb,
+                             p2, (int)M, (int)N, (int)K, gm);
+    if (e != cudaSuccess) return cuda_fail(e, "gemm_gather launch");
+    return MKQ_OK;
+}
+
+mkq_status mkq_wait_counter(const uint32_t* counter, uint32_t target, void* stream) {
+    if (!counter) return fail(MKQ_ERR_NULL, "counter");
+    mkq::wait_counter_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(counter, target);
+    cudaError_t e = cudaPeekAtLastError();
+    return e == cudaSuccess ? MKQ_OK : cuda_fail(e, "wait_counter launch");
+}
+
+typedef CUresult (*AddrRangeFn)(CUdeviceptr*, size_t*, CUdeviceptr);
+
+mkq_status mkq_ipc_get_handle(const void* dev_ptr, void* handle, int64_t* offset) {
+    if (!dev_ptr || !handle || !offset) return fail(MKQ_ERR_NULL, "dev_ptr / handle / offset");
+    static AddrRangeFn range = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        return cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+                       q == cudaDriverEntryPointSuccess
+                   ? reinterpret_cast<AddrRangeFn>(p)
+                   : nullptr;
+    }();
+    if (!range) return fail(MKQ_ERR_CUDA, "cuMemGetAddressRange unavailable");
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    CUresult r = range(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr));
+    if (r != CUDA_SUCCESS) return fail(MKQ_ERR_CUDA, "cuMemGetAddressRange failed (%d)", (int)r);
+    cudaIpcMemHandle_t h;
+    cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
+    memcpy(handle, &h, sizeof(h));
+    *offset = (int64_t)(reinterpret_cast<CUdeviceptr>(dev_ptr) - base);
+    return MKQ_OK;
+}
+
+mkq_status mkq_ipc_open_handle(const void* handle, void** dev_ptr) {
+    if (!dev_ptr || !handle) return fail(MKQ_ERR_NULL, "dev_ptr / handle");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    cudaError_t e = cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess);
+    return e == cudaSuccess ? MKQ_OK : cuda_fail(e, "cudaIpcOpenMemHandle");
+}
+
+mkq_status mkq_ipc_close(void* dev_ptr) {
+    cudaError_t e = cudaIpcCloseMemHandle(dev_ptr);
+    return e == cudaSuccess ? MKQ_OK : cuda_fail(e, "cudaIpcCloseMemHandle");
+}
+
 size_t mkq_gemm_workspace_size(int64_t, int64_t, int64_t) { return 0; }
 
 size_t mkq_gemm_residual_ln_workspace_size(int64_t M, int64_t N) {

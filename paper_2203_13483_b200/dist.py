@@ -123,6 +123,70 @@ class ColumnParallelFFN:
         return self.gemm(a2_full, self.w2, L.scales["s_ffn2_in"], self.sw2, self.b2, mode=M.OUT_F32, K=L.ffn,
                          stream=stream)
 
+    # ---------------------------------------------------------------- NEXT(4) fused all-gather
+    def setup_fused_gather(self, T: int, group=None) -> None:
+        """Allocate this rank's gathered FFN2-input buffer [T, F/2] (packed
+        int4) and its arrival counter, exchange CUDA-IPC handles with the
+        other ranks (dist.all_gather_object) and map theirs.  After this,
+        forward_fused writes every rank's FFN1 column block straight into
+        every rank's buffer from the GEMM epilogue (mkq_gemm_w4a4_gather):
+        no NCCL call and no interleave for the first all-gather."""
+        M, L = self.M, self.layer
+        if L.bits != 4 or self.Fl % 256 or L.hidden > 1024:
+            raise ValueError("fused all-gather: W4A4 layers with F/world % 256 == 0 and hidden <= 1024")
+        dev = L.t["w_1"].device
+        self.T_fused = T
+        self.gbuf = torch.zeros((T, L.ffn // 2), dtype=torch.uint8, device=dev)
+        self.counter = torch.zeros(64, dtype=torch.int32, device=dev)   # [0] used; 256-byte slot
+        self.arrivals = M.mkq_gemm_gather_arrivals(T, self.Fl)
+        self.epoch = 0
+        mine = (M.mkq_ipc_get_handle(self.gbuf), M.mkq_ipc_get_handle(self.counter))
+        if self.world > 1:
+            allh = [None] * self.world
+            dist.all_gather_object(allh, mine, group=group)
+        else:
+            allh = [mine]
+        self._mapped = []
+        outs, cnts = [], []
+        for r, ((hb, ob), (hc, oc)) in enumerate(allh):
+            if r == self.rank:
+                outs.append(self.gbuf.data_ptr())
+                cnts.append(self.counter.data_ptr())
+                continue
+            bb, bc = M.mkq_ipc_open_handle(hb), M.mkq_ipc_open_handle(hc)
+            self._mapped += [bb, bc]
+            outs.append(bb + ob)
+            cnts.append(bc + oc)
+        self.outs, self.cnts = outs, cnts
+
+    def close_fused_gather(self) -> None:
+        for b in getattr(self, "_mapped", []):
+            self.M.mkq_ipc_close(b)
+        self._mapped = []
+
+    def forward_fused(self, codes_h1: torch.Tensor, h1: torch.Tensor,
+                      gather: Optional[Callable[[torch.Tensor], torch.Tensor]] = None, stream=None) -> torch.Tensor:
+        """forward() with the FFN1 all-gather fused into the FFN1 GEMM.  The
+        caller's ranks must all call it (the counters count every rank's
+        CTAs).  Reuse of the gathered buffers across calls is ordered by the
+        second all-gather: a rank can only pass it once every rank's FFN2
+        (the reader of its buffer) has run."""
+        M, L = self.M, self.layer
+        gather = gather or (lambda x: gather_blocks(x, self.world))
+        T = h1.shape[0]
+        assert T == self.T_fused, "setup_fused_gather(T) for this token count"
+        self.epoch += 1
+        M.mkq_gemm_w4a4_gather(codes_h1, self.w1, L.scales["s_ffn1_in"], self.sw1, self.b1, self.outs, self.cnts,
+                               col0=self.rank * self.Fl, ldo=L.ffn // 2, s_out=L.scales["s_ffn2_in"], gelu=True,
+                               qmin=self.lo, qmax=self.hi, K=L.hidden,
+                               requant_table=L.table if L.table is not None else None, stream=stream)
+        M.mkq_wait_counter(self.counter.data_ptr(), self.epoch * self.world * self.arrivals, stream=stream)
+        f_loc = self.ffn2_local(self.gbuf, stream)                   # [T, hl] fp32
+        f_blocks = gather(f_loc)                                     # [g, T, hl]
+        f = M.mkq_interleave_blocks(f_blocks.view(torch.uint8), self.world, T, self.hl * 4,
+                                    stream=stream).view(torch.float32)
+        return M.mkq_residual_layernorm(f, h1, L.t["ln2_g"], L.t["ln2_b"], L.ln_eps, stream=stream)
+
     def forward(self, codes_h1: torch.Tensor, h1: torch.Tensor,
                 gather: Optional[Callable[[torch.Tensor], torch.Tensor]] = None, stream=None) -> torch.Tensor:
         """codes_h1 [T, K-codes] and h1 [T, h] fp32 on every rank -> h_out [T, h]."""

@@ -7,7 +7,7 @@ from __future__ import annotations
 
 import ctypes
 from collections import OrderedDict
-from typing import Optional
+from typing import Optional, Tuple
 
 import torch
 
@@ -189,6 +189,60 @@ def mkq_gemm_w8a8(a: torch.Tensor, w: torch.Tensor, s_a: float, s_w: torch.Tenso
     K = K if K is not None else a.shape[1]
     return _gemm("mkq_gemm_w8a8", a, w, K, s_a, s_w, bias, mode, gelu, s_out, qmin, qmax, out, stream,
                  requant_table)
+
+
+def mkq_gemm_gather_arrivals(M: int, N: int) -> int:
+    """Counter increments one mkq_gemm_w4a4_gather launch adds per buffer."""
+    return int(lib().mkq_gemm_gather_arrivals(M, N))
+
+
+def mkq_gemm_w4a4_gather(a: torch.Tensor, w: torch.Tensor, s_a: float, s_w: torch.Tensor,
+                         bias: Optional[torch.Tensor], outs, counters, col0: int, ldo: int, s_out: float,
+                         gelu: bool = True, qmin: int = -8, qmax: int = 7, K: Optional[int] = None,
+                         requant_table=None, stream=None) -> None:
+    """NEXT(4) fused all-gather: the int4-requant W4A4 linear whose tiles land
+    in every rank's gathered buffer (mkq_gemm_w4a4_gather).  outs / counters
+    are device addresses (ints) valid in this process: local tensors'
+    data_ptr() or CUDA-IPC mappings of the peers' buffers."""
+    M, N = a.shape[0], w.shape[0]
+    K = K if K is not None else a.shape[1] * 2
+    if requant_table is None:
+        requant_table = mkq_requant_table(gelu, s_out, qmin, qmax, a.device, stream)
+    epi = MkqEpilogue(OUT_I4, int(gelu), float(s_out), qmin, qmax, requant_table.data_ptr())
+    n = len(outs)
+    if len(counters) != n:
+        raise ValueError("one counter per gathered buffer")
+    outs_c = (ctypes.c_void_p * n)(*[int(o) for o in outs])
+    cnt_c = (ctypes.c_void_p * n)(*[int(c) for c in counters])
+    check("mkq_gemm_w4a4_gather", lib().mkq_gemm_w4a4_gather(
+        _ptr(a), _row_bytes(a), _ptr(w), _row_bytes(w), M, N, K, float(s_a), _ptr(s_w), _ptr(bias),
+        ctypes.byref(epi), outs_c, n, int(col0), int(ldo), cnt_c, _stream(stream)))
+
+
+def mkq_wait_counter(counter: int, target: int, stream=None) -> None:
+    """Block `stream` until the uint32 at device address `counter` >= target."""
+    check("mkq_wait_counter", lib().mkq_wait_counter(ctypes.c_void_p(int(counter)), target & 0xFFFFFFFF,
+                                                     _stream(stream)))
+
+
+def mkq_ipc_get_handle(t: torch.Tensor) -> Tuple[bytes, int]:
+    """(64-byte CUDA IPC handle of the allocation holding t, t's byte offset in it)."""
+    buf = ctypes.create_string_buffer(64)
+    off = ctypes.c_int64()
+    check("mkq_ipc_get_handle", lib().mkq_ipc_get_handle(_ptr(t), buf, ctypes.byref(off)))
+    return buf.raw, int(off.value)
+
+
+def mkq_ipc_open_handle(handle: bytes) -> int:
+    """Map a peer's allocation; returns its base device address in this process."""
+    ptr = ctypes.c_void_p()
+    check("mkq_ipc_open_handle", lib().mkq_ipc_open_handle(ctypes.create_string_buffer(bytes(handle), 64),
+                                                           ctypes.byref(ptr)))
+    return int(ptr.value)
+
+
+def mkq_ipc_close(base: int) -> None:
+    check("mkq_ipc_close", lib().mkq_ipc_close(ctypes.c_void_p(int(base))))
 
 
 _LN_WS = {}
