@@ -929,10 +929,9 @@ mkq_status mkq_attention(const void* qkv, int64_t ld, int64_t batch, int64_t max
     }
     mkq_status s = check_device();
     if (s != MKQ_OK) return s;
-    static const int attn_env = [] {   // MKQ_ATTN=tc|mma|pp forces a kernel (diagnostics)
+    static const int attn_env = [] {   // MKQ_ATTN=mma|pp forces a kernel (diagnostics)
         const char* v = getenv("MKQ_ATTN");
         if (v && strcmp(v, "mma") == 0) return 1;
-        if (v && strcmp(v, "tc") == 0) return 0;
         if (v && strcmp(v, "pp") == 0) return 2;
         return -1;
     }();
@@ -981,41 +980,6 @@ mkq_status mkq_attention(const void* qkv, int64_t ld, int64_t batch, int64_t max
         const int grid = (int)(nitems < sms ? nitems : sms);   // persistent, 1 CTA per SM
         launch_k(kern, dim3(grid), dim3(mkq::attnpp::kThreads), mkq::attnpp::kSmem, st, 1, mq, mkv, p, heads, pairs,
                  (int)nitems);
-    } else if (attn_path == 0) {
-        static bool attr_set[64] = {};
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (!attr_set[dev]) {
-            cudaError_t e = cudaFuncSetAttribute(mkq::attn2::attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 mkq::attn2::kSmem);
-            if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(attn)");
-            attr_set[dev] = true;
-        }
-        CUtensorMap mq, mkv;
-        s = make_map_t(&mq, qkv, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, (uint64_t)(3 * hidden), (uint64_t)tokens,
-                       (uint64_t)ld * 2, 64, mkq::attn2::kBQ, CU_TENSOR_MAP_SWIZZLE_128B);
-        if (s != MKQ_OK) return s;
-        s = make_map_t(&mkv, qkv, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, (uint64_t)(3 * hidden), (uint64_t)tokens,
-                       (uint64_t)ld * 2, 64, mkq::attn2::kBK, CU_TENSOR_MAP_SWIZZLE_128B);
-        if (s != MKQ_OK) return s;
-        mkq::attn2::Params p;
-        p.cu = cu;
-        p.seq = (int)max_seq;
-        p.hidden = (int)hidden;
-        p.out_mode = out_mode;
-        p.s_out = s_out;
-        p.qmin = qmin;
-        p.qmax = qmax;
-        p.out = out;
-        p.ldo = ldo;
-        int sms = 0;
-        check_device(&sms);
-        const int qtiles = (int)((max_seq + mkq::attn2::kBQ - 1) / mkq::attn2::kBQ);
-        const int64_t nitems = (int64_t)batch * heads * qtiles;
-        if (nitems > (1ll << 30)) return fail(MKQ_ERR_SHAPE, "too many attention work items");
-        const int grid = (int)(nitems < 2 * sms ? nitems : 2 * sms);   // persistent, 2 CTAs per SM
-        mkq::attn2::attn_tc_kernel<<<grid, mkq::attn2::kThreads, mkq::attn2::kSmem, st>>>(mq, mkv, p, heads, qtiles,
-                                                                                          (int)nitems);
     } else {
     mkq::attn::Params p;
     p.qkv = static_cast<const __half*>(qkv);
