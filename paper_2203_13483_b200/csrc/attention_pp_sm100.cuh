@@ -287,10 +287,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int cc = 0; cc < 4; ++cc)
                     for (int i = 0; i < 32; ++i) sv[cc][i] = __float_as_uint((float)((lane * 7 + i * 3 + cc) & 15));
 #else
-                // one 32-column load in flight per warp: tools/tmem_bench.cu measures
-                // 56 B/cycle/SM for ld.x32 + wait but 32 B/cycle/SM when a warp
-                // issues four x32 loads before waiting (profiles/r02_tmem_bench.md),
-                // and this readback is the kernel's bound
+                // 32 columns per load (a 4 KB x32 load costs a warp ~94 cycles with
+                // or without others in flight: profiles/r02_microbench.md)
                 for (int cc = 0; cc < 4; ++cc) {
                     ptx::tmem_ld_32x32b_x32(tS(x) + lane_off + 32 * cc, sv[cc]);
                     ptx::tmem_ld_wait_regs(sv[cc]);

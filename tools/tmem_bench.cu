@@ -15,6 +15,16 @@ __device__ __forceinline__ void ld32(uint32_t taddr, uint32_t (&r)[32]) {
           "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
         : "r"(taddr));
 }
+
+// folds all 32 results (a dynamically indexed r[it & 31] would put the array
+// in local memory and time the local stores instead of the TMEM reads; an
+// empty asm "use" lets ptxas delete the unused loads)
+__device__ __forceinline__ uint32_t fold(const uint32_t (&r)[32]) {
+    uint32_t x = 0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) x ^= r[i];   // 3-input LOP3s: ~16 ALU ops per 32 registers
+    return x;
+}
 __device__ __forceinline__ void st32(uint32_t taddr, const uint32_t (&r)[32]) {
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
@@ -75,7 +85,7 @@ __global__ void k(int iters, uint32_t* out, long long* cyc) {
         if (MODE == 0) {
             ld32(base, r);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            acc ^= r[it & 31];
+            acc ^= fold(r);
         } else if (MODE == 1) {
             uint32_t a[32], b[32], c[32];
             ld32(base, r);
@@ -83,11 +93,11 @@ __global__ void k(int iters, uint32_t* out, long long* cyc) {
             ld32(base ^ 128, b);
             ld32(base ^ 192, c);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            acc ^= r[it & 31] ^ a[(it + 1) & 31] ^ b[(it + 2) & 31] ^ c[(it + 3) & 31];
+            acc ^= fold(r) ^ fold(a) ^ fold(b) ^ fold(c);
         } else if (MODE == 5) {
             ld32(base + 32u * (uint32_t)((it + (warp >> 2)) & 7), r);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            acc ^= r[it & 31];
+            acc ^= fold(r);
         } else if (MODE == 6) {
             uint32_t a[32], b[32], c[32];
             const uint32_t b0 = slot + ((uint32_t)((warp & 3) * 32) << 16) + 128u * (uint32_t)((it + (warp >> 2)) & 3);
@@ -96,24 +106,24 @@ __global__ void k(int iters, uint32_t* out, long long* cyc) {
             ld32(b0 + 64, b);
             ld32(b0 + 96, c);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            acc ^= r[it & 31] ^ a[(it + 1) & 31] ^ b[(it + 2) & 31] ^ c[(it + 3) & 31];
+            acc ^= fold(r) ^ fold(a) ^ fold(b) ^ fold(c);
         } else if (MODE == 7) {
             uint32_t a[32];
             const uint32_t b0 = slot + ((uint32_t)((warp & 3) * 32) << 16) + 64u * (uint32_t)((it + (warp >> 2)) & 7);
             ld32(b0, r);
             ld32(b0 + 32, a);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            acc ^= r[it & 31] ^ a[(it + 1) & 31];
+            acc ^= fold(r) ^ fold(a);
         } else if (MODE == 3) {
             ld16x256_x8(base, r);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            acc ^= r[it & 31];
+            acc ^= fold(r);
         } else if (MODE == 4) {
             ld16x128_x16(base, r);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            acc ^= r[it & 31];
+            acc ^= fold(r);
         } else {
-            r[it & 31] += 1;
+            r[0] += 1;   // static index: r stays in registers
             st32(base, r);
             if ((it & 3) == 3) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         }

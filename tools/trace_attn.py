@@ -10,7 +10,7 @@ import ctypes, os, subprocess, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2203_13483_b200 import build as B
-dbg = os.path.join(ROOT, "build_dbg", "libmkq.so")
+dbg = os.environ.get("TRACE_LIB") or os.path.join(ROOT, "build_dbg", "libmkq.so")
 if not os.environ.get("NO_BUILD"):
     os.makedirs(os.path.dirname(dbg), exist_ok=True)
     extra = os.environ.get("EXTRA_FLAGS", "").split()
