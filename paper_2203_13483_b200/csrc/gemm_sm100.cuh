@@ -151,6 +151,9 @@ __device__ __forceinline__ void epilogue_acc(const EpiParams& ep, const int32_t 
         const float b = kSmemScales ? b_s[i] : (hb ? __ldg(ep.bias + n + i) : 0.0f);
         y[i] = dequant(acc[i], sc, b, hb);
     }
+#ifdef MKQ_ABL_NOSTORE   // ablation (diagnostics only): no global stores
+    if (y[0] != 1234.5f) return;
+#endif
     epilogue_emit(ep, y, orow, n);
 }
 
@@ -160,6 +163,81 @@ __device__ __forceinline__ void epilogue_store(const EpiParams& ep, const uint32
 #pragma unroll
     for (int i = 0; i < 32; ++i) acc[i] = kInt4 ? ((int32_t)v[i] >> 8) : (int32_t)v[i];
     epilogue_acc<false>(ep, acc, row, n, nullptr, nullptr);
+}
+
+// Small-M direct epilogue: one row's 32 outputs (columns n..n+31) -> the
+// TMA-store staging boxes of one warp (32 rows).  Box layout per output mode
+// (make_out_map in mkq_abi.cu): f32/i32 two boxes of 16 columns (64 B rows,
+// SWIZZLE_64B), f16/bf16 one of 32 columns (64 B, SWIZZLE_64B), i8 32 B rows
+// (SWIZZLE_32B), i4 16 B rows (no swizzle); boxes are 2 KB apart.  Same
+// arithmetic as epilogue_acc/epilogue_emit (R4, R7, R11, Eq.1).
+__device__ __forceinline__ uint32_t stage_off(int r, int c, int P) {
+    const int f = P == 64 ? ((r >> 1) & 3) : (P == 32 ? ((r >> 2) & 1) : 0);
+    return (uint32_t)(r * P + ((c ^ f) << 4));
+}
+__device__ __forceinline__ int stage_boxes(int mode) { return mode == OUT_F32 || mode == OUT_I32 ? 2 : 1; }
+__device__ __forceinline__ void epilogue_acc_stage(const EpiParams& ep, const int32_t (&acc)[32], const float* sc_s,
+                                                   const float* b_s, uint8_t* stage, int r) {
+    if (ep.mode == OUT_I32) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            *reinterpret_cast<int4*>(stage + (k >> 2) * 2048 + stage_off(r, k & 3, 64)) =
+                make_int4(acc[4 * k], acc[4 * k + 1], acc[4 * k + 2], acc[4 * k + 3]);
+        return;
+    }
+    float y[32];
+    const bool hb = ep.bias != nullptr;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) y[i] = dequant(acc[i], sc_s[i], b_s[i], hb);
+    if (ep.gelu) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) y[i] = gelu_pinned(y[i]);
+    }
+    switch (ep.mode) {
+    case OUT_F32:
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            *reinterpret_cast<float4*>(stage + (k >> 2) * 2048 + stage_off(r, k & 3, 64)) =
+                make_float4(y[4 * k], y[4 * k + 1], y[4 * k + 2], y[4 * k + 3]);
+        break;
+    case OUT_BF16:
+    case OUT_F16: {
+        uint32_t w[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+            w[i] = ep.mode == OUT_BF16 ? pack_bf16x2(y[2 * i], y[2 * i + 1]) : pack_f16x2(y[2 * i], y[2 * i + 1]);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            *reinterpret_cast<uint4*>(stage + stage_off(r, k, 64)) = make_uint4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
+        break;
+    }
+    case OUT_I4: {
+        uint32_t w[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            int q[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) q[j] = quant_code(y[8 * i + j], ep.s_out, ep.qmin, ep.qmax);
+            w[i] = pack_nib8(q);
+        }
+        *reinterpret_cast<uint4*>(stage + stage_off(r, 0, 16)) = make_uint4(w[0], w[1], w[2], w[3]);
+        break;
+    }
+    case OUT_I8: {
+        uint32_t w[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            w[i] = pack_byte4(quant_code(y[4 * i], ep.s_out, ep.qmin, ep.qmax),
+                              quant_code(y[4 * i + 1], ep.s_out, ep.qmin, ep.qmax),
+                              quant_code(y[4 * i + 2], ep.s_out, ep.qmin, ep.qmax),
+                              quant_code(y[4 * i + 3], ep.s_out, ep.qmin, ep.qmax));
+        *reinterpret_cast<uint4*>(stage + stage_off(r, 0, 32)) = make_uint4(w[0], w[1], w[2], w[3]);
+        *reinterpret_cast<uint4*>(stage + stage_off(r, 1, 32)) = make_uint4(w[4], w[5], w[6], w[7]);
+        break;
+    }
+    default:
+        break;
+    }
 }
 
 #ifdef MKQ_TTRACE
@@ -185,7 +263,7 @@ __device__ unsigned long long* g_ttrace = nullptr;
 template <class Cfg, bool kCl = false>
 __global__ void __launch_bounds__(Cfg::kThreads, 1)
     gemm_i8tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     const EpiParams ep, int M, int N, int K, int splits) {
+                     const __grid_constant__ CUtensorMap tmO, const EpiParams ep, int M, int N, int K, int splits) {
     constexpr int BM = Cfg::BM, BN = Cfg::BN, S8 = Cfg::S8, SP = Cfg::SP;
     constexpr bool kInt4 = Cfg::kInt4;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -344,6 +422,34 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
                 ptx::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + ab * BN + 32 * j, v);
                 ptx::tmem_ld_wait();
                 if constexpr (kCl) {
+                  if (splits == 1) {
+                    // no K split: epilogue straight from TMEM (no cluster
+                    // barrier, no DSMEM round trip); scales/bias staged by warp 3
+                    // Rows are staged in the idle int8 ring (every MMA of this
+                    // CTA's only tile has completed) and TMA-stored per warp: a
+                    // row-per-lane STG scatters 32 rows per instruction and cost
+                    // ~2 us per tile at Table-2 sizes (tools/trace_small.py).
+                    if (j == 0) ptx::named_bar_sync(1, 160);
+                    if (threadIdx.x == 128 && j == 0) TTRACE(8);
+                    int32_t acc[32];
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) acc[i] = kInt4 ? ((int32_t)v[i] >> 8) : (int32_t)v[i];
+                    uint8_t* stage = ring8 + (q * (BN / 32) + j) * 4096;
+                    epilogue_acc_stage(ep, acc, sc_s + 32 * j, b_s + 32 * j, stage, lane);
+                    ptx::fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        const int y0 = m0 + q * 32;
+                        if (ep.mode == OUT_F32 || ep.mode == OUT_I32) {
+                            ptx::tma_store_2d(&tmO, stage, n, y0);
+                            ptx::tma_store_2d(&tmO, stage + 2048, n + 16, y0);
+                        } else {
+                            ptx::tma_store_2d(&tmO, stage, ep.mode == OUT_I4 ? n / 2 : n, y0);
+                        }
+                        ptx::tma_store_commit();
+                    }
+                    if (threadIdx.x == 128 && j == 0) TTRACE(15);
+                  } else {
                     // stage the (shifted) partial of row q*32+lane in the idle int8 ring
                     uint8_t* dst = ring8 + (q * 32 + lane) * kRP + j * 128;
 #pragma unroll
@@ -355,10 +461,12 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
                         t.w = kInt4 ? (uint32_t)((int32_t)v[4 * i + 3] >> 8) : v[4 * i + 3];
                         *reinterpret_cast<uint4*>(dst + 16 * i) = t;
                     }
+                  }
                 } else if (row < M) {
                     epilogue_store<kInt4>(ep, v, row, n);
                 }
             }
+            if (kCl && splits == 1 && lane == 0) ptx::tma_store_wait_read<0>();   // staging is read before exit
             ptx::tc_fence_before();
             ptx::mbar_arrive(&tempty[ab]);
             if (threadIdx.x == 128) TTRACE(7);
@@ -371,6 +479,7 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
             sc_s[c] = n < N ? __fmul_rn(ep.s_a, __ldg(ep.s_w + n)) : 0.0f;
             b_s[c] = (n < N && ep.bias) ? __ldg(ep.bias + n) : 0.0f;
         }
+        if (splits == 1) ptx::named_bar_arrive(1, 160);   // -> the epilogue warps
     } else if (kInt4 && warp >= 8) {
         // ---------------------------------------------------- int4 -> int8 unpack
         const int u = threadIdx.x - 256;
@@ -382,34 +491,49 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
             // so four stages are expanded in parallel instead of four warps
             // sharing each stage in turn (stage spacing was 0.45 us for int4
             // against 0.32 us of TMA for int8, tools/trace_small.py).
-            static_assert(Cfg::SP == 4 && Cfg::S8 == 4, "warp-per-stage unpack");
+            static_assert(Cfg::SP % 4 == 0 && Cfg::S8 == 4, "warp-per-stage unpack");
             const int w = warp - 8;
             int kb0, kb1;
             k_range(blockIdx.x, kb0, kb1);
             for (int j = w; kb0 + j < kb1; j += 4) {
                 const uint32_t ph = (uint32_t)(j >> 2) & 1u;
-                ptx::mbar_wait(&fullP[w], ph);
+                const int sp = j % Cfg::SP;   // packed slot (slot sp is only ever used by warp sp % 4)
+                ptx::mbar_wait(&fullP[sp], (uint32_t)(j / Cfg::SP) & 1u);
                 ptx::mbar_wait(&empty8[w], ph ^ 1);
-                const uint8_t* src = ringP + w * Cfg::kStageP;
+                const uint8_t* src = ringP + sp * Cfg::kStageP;
                 uint8_t* dst = ring8 + w * Cfg::kStage8;
-#pragma unroll 6
-                for (int i = 0; i < kChunks / 32; ++i) {
-                    const int id = lane + 32 * i;
-                    const int r = id >> 2, c = id & 3;
-                    const uint4 p = *reinterpret_cast<const uint4*>(src + r * 64 + c * 16);
-                    uint4 lo, hi;
-                    lo.x = (p.x << 4) & 0xF0F0F0F0u; hi.x = p.x & 0xF0F0F0F0u;
-                    lo.y = (p.y << 4) & 0xF0F0F0F0u; hi.y = p.y & 0xF0F0F0F0u;
-                    lo.z = (p.z << 4) & 0xF0F0F0F0u; hi.z = p.z & 0xF0F0F0F0u;
-                    lo.w = (p.w << 4) & 0xF0F0F0F0u; hi.w = p.w & 0xF0F0F0F0u;
-                    const int r7 = r & 7;
-                    uint8_t* drow = dst + r * 128;
-                    *reinterpret_cast<uint4*>(drow + (((2 * c) ^ r7) << 4)) = lo;
-                    *reinterpret_cast<uint4*>(drow + (((2 * c + 1) ^ r7) << 4)) = hi;
+                // Lane handles chunk c = lane & 3 of rows r0 + 8 i: the swizzle
+                // phase and both destination offsets are loop invariants.  All
+                // loads of a batch are issued before its stores (through generic
+                // pointers the compiler cannot hoist a load above a possibly
+                // aliasing store: one LDS -> STS round trip per chunk made a stage
+                // cost one warp ~1 us, tools/trace_small.py).
+                constexpr int kPer = kChunks / 32, kBatch = 12;
+                static_assert(kPer % kBatch == 0, "unpack batches");
+                const uint32_t r0 = (uint32_t)lane >> 2, c = (uint32_t)lane & 3u, r7 = r0 & 7u;
+                const uint32_t s0 = ptx::smem_u32(src) + r0 * 64u + c * 16u;
+                const uint32_t d0 = ptx::smem_u32(dst) + r0 * 128u;
+                const uint32_t dlo = ((2u * c) ^ r7) << 4, dhi = ((2u * c + 1u) ^ r7) << 4;
+#pragma unroll
+                for (int b = 0; b < kPer; b += kBatch) {
+                    uint4 pk[kBatch];
+#pragma unroll
+                    for (int i = 0; i < kBatch; ++i) pk[i] = ptx::lds128(s0 + (uint32_t)(b + i) * 512u);
+#pragma unroll
+                    for (int i = 0; i < kBatch; ++i) {
+                        uint4 lo, hi;
+                        ptx::unpack_i4x8(pk[i].x, lo.x, hi.x);
+                        ptx::unpack_i4x8(pk[i].y, lo.y, hi.y);
+                        ptx::unpack_i4x8(pk[i].z, lo.z, hi.z);
+                        ptx::unpack_i4x8(pk[i].w, lo.w, hi.w);
+                        const uint32_t rb = d0 + (uint32_t)(b + i) * 1024u;
+                        ptx::sts128(rb + dlo, lo);
+                        ptx::sts128(rb + dhi, hi);
+                    }
                 }
                 ptx::fence_proxy_async_smem();
                 ptx::mbar_arrive(&full8[w]);
-                ptx::mbar_arrive(&emptyP[w]);
+                ptx::mbar_arrive(&emptyP[sp]);
             }
             // tail: this slot's last MMA commit has landed
             const int jl = (kb1 - kb0 - 1 - w) >= 0 ? ((kb1 - kb0 - 1 - w) / 4) * 4 + w : -1;
@@ -454,7 +578,7 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
         }
     }
 
-    if constexpr (kCl) {
+    if (kCl && splits > 1) {
         // DSMEM reduce-scatter of the staged partials + epilogue (all warps)
         ptx::cluster_sync();   // release/acquire: every peer's staged rows are visible
         const int tile = blockIdx.x / splits;

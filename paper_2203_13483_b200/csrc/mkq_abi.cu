@@ -233,15 +233,21 @@ mkq_status launch_gemm(const void* a, int64_t lda, const void* w, int64_t ldw, i
     s = make_map(&mb, w, kbytes, (uint64_t)N, (uint64_t)ldw, box_in, Cfg::BN, !Cfg::kInt4);
     if (s != MKQ_OK) return s;
     const int tiles = ((M + Cfg::BM - 1) / Cfg::BM) * ((N + Cfg::BN - 1) / Cfg::BN);
+    // output map: TMA stores of the small-M plan's unsplit epilogue (unused otherwise)
+    CUtensorMap mo = ma;
+    if (kCl && splits == 1) {
+        s = make_out_map(&mo, ep.out, ep.mode, M, N, ep.ldo_bytes);
+        if (s != MKQ_OK) return s;
+    }
     cudaError_t e;
     if constexpr (kCl) {
         // one CTA per (tile, K split); the splits of a tile form one cluster
         e = launch_k(mkq::gemm_i8tc_kernel<Cfg, true>, dim3((unsigned)(tiles * splits)), dim3(Cfg::kThreads),
-                     Cfg::kSmem, st, splits, ma, mb, ep, M, N, K, splits);
+                     Cfg::kSmem, st, splits, ma, mb, mo, ep, M, N, K, splits);
     } else {
         const int grid = tiles < sms ? tiles : sms;
         e = launch_k(mkq::gemm_i8tc_kernel<Cfg, false>, dim3(grid), dim3(Cfg::kThreads), Cfg::kSmem, st, 1, ma, mb,
-                     ep, M, N, K, 1);
+                     mo, ep, M, N, K, 1);
     }
     if (e != cudaSuccess) return cuda_fail(e, "gemm launch");
     return MKQ_OK;

@@ -9,10 +9,11 @@ import ctypes, os, subprocess, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2203_13483_b200 import build as B
-dbg = os.path.join(ROOT, "build_dbg", "ttrace", "libmkq.so")
+extra = os.environ.get("EXTRA", "").split()   # e.g. EXTRA=-DMKQ_ABL_NOSTORE (ablation builds)
+dbg = os.path.join(ROOT, "build_dbg", "ttrace" + "".join(f.replace("-D", "_") for f in extra), "libmkq.so")
 if not os.environ.get("NO_BUILD"):
     os.makedirs(os.path.dirname(dbg), exist_ok=True)
-    subprocess.check_call([B.NVCC, *B.FLAGS, "-DMKQ_TTRACE", "-o", dbg, os.path.join(B.CSRC, "mkq_abi.cu"), "-ldl"])
+    subprocess.check_call([B.NVCC, *B.FLAGS, "-DMKQ_TTRACE", *extra, "-o", dbg, os.path.join(B.CSRC, "mkq_abi.cu"), "-ldl"])
 if os.environ.get("BUILD_ONLY"):
     sys.exit(0)
 os.environ["MKQ_LIB"] = dbg
