@@ -578,21 +578,27 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
         }
     }
 
-    if (kCl && splits > 1) {
+    if constexpr (kCl) if (splits > 1) {
         // DSMEM reduce-scatter of the staged partials + epilogue (all warps)
         ptx::cluster_sync();   // release/acquire: every peer's staged rows are visible
         const int tile = blockIdx.x / splits;
         const int m0 = (tile / n_tiles) * BM, n0 = (tile % n_tiles) * BN;
         const int rank = (int)ptx::cluster_ctarank();
-        const int rows_per = (BM + splits - 1) / splits;
-        const int r0 = rank * rows_per, r1 = min(BM, r0 + rows_per);
+        // CTA `rank` owns the 32-row groups grp = rank, rank + splits, ... of
+        // the tile; one warp per (group, 32-column block): lane = row, sums
+        // the peers' partials over DSMEM, stages the outputs and TMA-stores
+        // them (warp-private 4 KB staging slot past the partials)
         constexpr int kJ = BN / 32;
-        const int tasks = (r1 - r0) * kJ;
+        const int ngroups = (min(BM, M - m0) + 31) / 32;
+        const int owned = ngroups > rank ? (ngroups - rank + splits - 1) / splits : 0;
+        const int nwarps = (int)(blockDim.x >> 5);
         const uint32_t red0 = ptx::smem_u32(ring8);
-        for (int t = threadIdx.x; t < tasks; t += blockDim.x) {
-            const int rl = r0 + t / kJ, j = t % kJ;
-            const int row = m0 + rl, n = n0 + 32 * j;
-            if (row >= M || n >= N) continue;
+        static_assert(Cfg::BM * kRP <= 40960 && 40960 + (Cfg::kThreads / 32) * 4096 <= Cfg::S8 * Cfg::kStage8,
+                      "partials + per-warp staging fit the int8 ring");
+        uint8_t* stage = ring8 + 40960 + warp * 4096;
+        for (int u = warp; u < owned * kJ; u += nwarps) {
+            const int grp = rank + splits * (u / kJ), j = u % kJ;
+            const int rl = grp * 32 + lane, n = n0 + 32 * j;
             int32_t acc[32];
 #pragma unroll
             for (int i = 0; i < 32; ++i) acc[i] = 0;
@@ -611,8 +617,23 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
                     acc[4 * i + 2] += (int32_t)x[i].z; acc[4 * i + 3] += (int32_t)x[i].w;
                 }
             }
-            epilogue_acc<true>(ep, acc, row, n, sc_s + 32 * j, b_s + 32 * j);
+            if (lane == 0) ptx::tma_store_wait_read<0>();   // this warp's previous store has read the slot
+            __syncwarp();
+            epilogue_acc_stage(ep, acc, sc_s + 32 * j, b_s + 32 * j, stage, lane);
+            ptx::fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+                const int y0 = m0 + grp * 32;
+                if (ep.mode == OUT_F32 || ep.mode == OUT_I32) {
+                    ptx::tma_store_2d(&tmO, stage, n, y0);
+                    ptx::tma_store_2d(&tmO, stage + 2048, n + 16, y0);
+                } else {
+                    ptx::tma_store_2d(&tmO, stage, ep.mode == OUT_I4 ? n / 2 : n, y0);
+                }
+                ptx::tma_store_commit();
+            }
         }
+        if (lane == 0) ptx::tma_store_wait_read<0>();
         if (threadIdx.x == 128) TTRACE(8);
         ptx::cluster_sync();   // peers may still be reading this CTA's rows
     }

@@ -233,9 +233,9 @@ mkq_status launch_gemm(const void* a, int64_t lda, const void* w, int64_t ldw, i
     s = make_map(&mb, w, kbytes, (uint64_t)N, (uint64_t)ldw, box_in, Cfg::BN, !Cfg::kInt4);
     if (s != MKQ_OK) return s;
     const int tiles = ((M + Cfg::BM - 1) / Cfg::BM) * ((N + Cfg::BN - 1) / Cfg::BN);
-    // output map: TMA stores of the small-M plan's unsplit epilogue (unused otherwise)
+    // output map: TMA stores of the small-M plan's epilogues (unused otherwise)
     CUtensorMap mo = ma;
-    if (kCl && splits == 1) {
+    if (kCl) {
         s = make_out_map(&mo, ep.out, ep.mode, M, N, ep.ldo_bytes);
         if (s != MKQ_OK) return s;
     }
@@ -542,6 +542,12 @@ mkq_status gemm_common(bool int4, const void* a, int64_t lda, const void* w, int
             // (8 unpack warps with 88-register epilogue warps measured 7% slower)
             static const int lut4_epi = [] { const char* v = getenv("MKQ_LUT4_EPI"); return v ? atoi(v) : 16; }();
             if (many_epi && e.out == MKQ_OUT_I4 && p2.table && !no_lut4) {
+                // small M (paper Table 2: FFN1 at 440-681 tokens): 256 x 128 pair
+                // tiles put twice as many SMs on the GEMM as 256 x 256 ones
+                static const int lut128_pairs = [] { const char* v = getenv("MKQ_LUT128_PAIRS"); return v ? atoi(v) : -1; }();
+                const int64_t pairs256 = ((M + 255) / 256) * (N / 256);
+                if (pairs256 * 4 <= sms && (lut128_pairs < 0 || pairs256 <= lut128_pairs))
+                    return launch_gemm2<mkq::Gemm2Cfg<128, 8, 4, true>>(a, lda, w, ldw, (int)M, (int)N, (int)K, p2, sms, st);
                 if (lut4_epi == 8)
                     return launch_gemm2<mkq::Gemm2Cfg<256, 8, 4, true>>(a, lda, w, ldw, (int)M, (int)N, (int)K, p2, sms, st);
                 if (lut4_epi == 168)
