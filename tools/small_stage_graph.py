@@ -71,3 +71,22 @@ with torch.cuda.stream(st):
     torch.cuda.synchronize()
 res["layer_x20"] = round(e0.elapsed_time(e1) * 1e3 / (10 * R), 2)
 print(f"bits={bits} T={T} small={os.environ.get('MKQ_SMALL_M', 'auto')}:", res, "stage_sum", round(sum(v for k, v in res.items() if k != 'layer_x20'), 1), flush=True)
+# kernel-switch cost (diagnostics): pairs of different stages alternating in one graph vs each alone
+if os.environ.get("PAIRS"):
+    names = [n for n, _ in calls]
+    fn = dict(calls)
+    for a_, b_ in [("qkv", "o"), ("o", "ffn2"), ("qkv", "ffn2"), ("ln1", "ln2"), ("quant", "ln2")]:
+        with torch.cuda.stream(st):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=st):
+                for _ in range(R // 2):
+                    fn[a_](); fn[b_]()
+            g.replay(); torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            for _ in range(10):
+                g.replay()
+            e1.record(st)
+            torch.cuda.synchronize()
+        pair_us = e0.elapsed_time(e1) * 1e3 / (10 * (R // 2))
+        print(f"pair {a_}+{b_}: {pair_us:.2f} us alternating vs {res[a_] + res[b_]:.2f} alone-sum", flush=True)
