@@ -34,13 +34,20 @@ __global__ void __launch_bounds__(256) quantize_pack_vec_kernel(
             const float4 a0 = __ldcs(s0p), b0 = __ldcs(s0p + 1), a1 = __ldcs(s1p), b1 = __ldcs(s1p + 1);
             const float v0[8] = {a0.x, a0.y, a0.z, a0.w, b0.x, b0.y, b0.z, b0.w};
             const float v1[8] = {a1.x, a1.y, a1.z, a1.w, b1.x, b1.y, b1.z, b1.w};
-            int q0[8], q1[8];
-            quant_group_rcp(v0, Q_t, q0);
-            quant_group_rcp(v1, Q_t, q1);
             if constexpr (kBits == 4) {
-                *reinterpret_cast<uint32_t*>(q + r0 * ldq + (c0 >> 1)) = pack_nib8(q0);
-                *reinterpret_cast<uint32_t*>(q + r1 * ldq + (c1 >> 1)) = pack_nib8(q1);
+                // f32x2 reciprocal path; groups within 2^-18 of a rounding
+                // boundary take the out-of-line exact Eq.1 (issue-bound
+                // before: ncu issue 77%, profiles/r02_layer_kernels.md)
+                bool n0 = false, n1 = false;
+                uint32_t w0 = quant_nib8_fast(v0, Q_t, n0), w1 = quant_nib8_fast(v1, Q_t, n1);
+                if (__builtin_expect(n0, 0)) w0 = quant_nib8_exact(v0[0], v0[1], v0[2], v0[3], v0[4], v0[5], v0[6], v0[7], s_t, qmin, qmax);
+                if (__builtin_expect(n1, 0)) w1 = quant_nib8_exact(v1[0], v1[1], v1[2], v1[3], v1[4], v1[5], v1[6], v1[7], s_t, qmin, qmax);
+                *reinterpret_cast<uint32_t*>(q + r0 * ldq + (c0 >> 1)) = w0;
+                *reinterpret_cast<uint32_t*>(q + r1 * ldq + (c1 >> 1)) = w1;
             } else {
+                int q0[8], q1[8];
+                quant_group_rcp(v0, Q_t, q0);
+                quant_group_rcp(v1, Q_t, q1);
                 *reinterpret_cast<uint2*>(q + r0 * ldq + c0) =
                     make_uint2(pack_byte4(q0[0], q0[1], q0[2], q0[3]), pack_byte4(q0[4], q0[5], q0[6], q0[7]));
                 *reinterpret_cast<uint2*>(q + r1 * ldq + c1) =
