@@ -58,9 +58,17 @@ struct GemmCfg {
     static constexpr int BM = 128;
     static constexpr int BN = BN_;
     static constexpr bool kInt4 = kInt4_;
-    static constexpr int BK = 128;                  // K elements per block (=128 int8 bytes/row)
-    static constexpr int kA8 = BM * BK;             // int8 bytes of A per stage
-    static constexpr int kB8 = BN * BK;
+    // BN 64 int4 is the small-M plan (one tile per CTA, kTA): its A operand is
+    // unpacked into tensor memory and read by the MMA from there (shared memory
+    // carries the packed tiles and the unpacked W only), and a stage spans 256 K
+    // (128-byte packed rows): at Table-2 sizes a stage's time is set by the
+    // number of TMA rows in flight, not by bytes (int4 and int8 stages of 128 K
+    // both took ~0.35 us with 4 stages in flight, tools/trace_small.py), so
+    // 256-K int4 stages halve the time per K
+    static constexpr bool kTA = kInt4 && BN == 64;
+    static constexpr int BK = kTA ? 256 : 128;      // K elements per block (=128 int8 bytes/row otherwise)
+    static constexpr int kA8 = kTA ? 0 : BM * BK;   // int8 bytes of A per stage (kTA: A lives in TMEM)
+    static constexpr int kB8 = BN * BK;             // (kTA: BK/128 SW128 sub-tiles of BN x 128 B)
     static constexpr int kStage8 = kA8 + kB8;
     static constexpr int kAP = BM * BK / 2;         // packed bytes of A per stage
     static constexpr int kBP = BN * BK / 2;
@@ -69,7 +77,10 @@ struct GemmCfg {
     static constexpr int SP = kInt4 ? (BN == 256 ? 3 : 4) : 0;
     static_assert(BN == 64 || BN == 128 || BN == 256, "BN");
     static constexpr int kThreads = kInt4 ? 384 : 256;
-    static constexpr uint32_t kTmemCols = 2 * BN;   // double-buffered accumulator
+    static constexpr uint32_t kTaCol = 128;         // first A column (kTA): accumulator in [0, 64)
+    static constexpr uint32_t kTaStageCols = BK / 4;   // A columns per stage (4 K bytes per column)
+    static constexpr uint32_t kTmemCols = kTA ? 512 : 2 * BN;   // (otherwise a double-buffered accumulator)
+    static_assert(!kTA || kTaCol + S8 * kTaStageCols <= kTmemCols, "TMEM budget");
     static constexpr int kBarBytes = 8 * (2 * S8 + 2 * SP + 4) + 16;
     static constexpr int kSmem = 1024 + S8 * kStage8 + SP * kStageP + kBarBytes;
     static_assert(kSmem <= 232448, "shared memory budget");
@@ -302,14 +313,15 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
     static_assert(!kCl || Cfg::BM * kRP <= Cfg::S8 * Cfg::kStage8, "partial staging fits the int8 ring");
     __shared__ float sc_s[kCl ? Cfg::BN : 1], b_s[kCl ? Cfg::BN : 1];
 
+    static_assert(!Cfg::kTA || kCl, "A in TMEM: one tile per CTA (small-M plan)");
     if (threadIdx.x == 0) {
         for (int i = 0; i < S8; ++i) {
-            ptx::mbar_init(&full8[i], kInt4 ? (kCl ? 32 : 128) : 1);
+            ptx::mbar_init(&full8[i], Cfg::kTA ? 4 : (kInt4 ? (kCl ? 32 : 128) : 1));
             ptx::mbar_init(&empty8[i], 1);
         }
         for (int i = 0; i < SP; ++i) {
             ptx::mbar_init(&fullP[i], 1);
-            ptx::mbar_init(&emptyP[i], kCl ? 32 : 128);
+            ptx::mbar_init(&emptyP[i], Cfg::kTA ? 4 : (kCl ? 32 : 128));
         }
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(&tfull[i], 1);
@@ -392,9 +404,18 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
                     if (lane == 0 && kb > kb0 && kb - kb0 < 7) TTRACE(9 + kb - kb0);
                     const uint64_t da = dA0 + (uint64_t)((s * Cfg::kStage8) >> 4);
                     const uint64_t db = da + (uint64_t)(Cfg::kA8 >> 4);
+                    if constexpr (Cfg::kTA) {   // A stage s in TMEM: 8 columns per 32-byte K step;
+                        // W: K step k in SW128 sub-tile k/4 (BN x 128 B each), 32 B apart inside it
+                        const uint32_t ta = tmem_base + Cfg::kTaCol + Cfg::kTaStageCols * (uint32_t)s;
+#pragma unroll
+                        for (int k = 0; k < Cfg::BK / 32; ++k)
+                            ptx::mma_i8_ts_warp(d, ta + 8u * k, db + (uint64_t)((k >> 2) * ((BN * 128) >> 4) + 2 * (k & 3)),
+                                                idesc, (kb != kb0) || k != 0);
+                    } else {
 #pragma unroll
                     for (int k = 0; k < Cfg::BK / 32; ++k)
                         ptx::mma_i8_ss_warp(d, da + 2 * k, db + 2 * k, idesc, (kb != kb0) || k != 0);
+                    }
                     ptx::mma_commit_warp(&empty8[s]);
                     if (++s == S8) { s = 0; ph ^= 1; }
                 }
@@ -485,59 +506,81 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
         const int u = threadIdx.x - 256;
         constexpr int kChunks = (BM + BN) * (Cfg::BK / 32);   // 16-byte packed chunks / stage
         static_assert(kChunks % 128 == 0, "chunk split");
-        if constexpr (kCl && kInt4) {
-            // Small-M plan (one unit per CTA, SP == S8 == 4 == unpack warps):
-            // unpack warp w owns ring slot w and unpacks whole stages w, w+4, ...,
-            // so four stages are expanded in parallel instead of four warps
-            // sharing each stage in turn (stage spacing was 0.45 us for int4
-            // against 0.32 us of TMA for int8, tools/trace_small.py).
-            static_assert(Cfg::SP % 4 == 0 && Cfg::S8 == 4, "warp-per-stage unpack");
-            const int w = warp - 8;
+        if constexpr (Cfg::kTA) {
+            // Small-M plan, A in TMEM: unpack warp q = warp % 4 owns TMEM lane
+            // quadrant q, i.e. A rows 32q..32q+31 of every stage (lane = row;
+            // packed A arrives with the TMA 128-byte swizzle, so the lanes' row
+            // reads are conflict-free), expands its row's 128 packed bytes in
+            // registers and stores the 256 int8 K bytes with two tcgen05.st
+            // (columns 8c..8c+3 = even codes of packed chunk c, 8c+4..8c+7 = odd
+            // codes: the permutation W gets in shared memory); and it unpacks
+            // W rows 16q..16q+15 into the SW128 sub-tiles (K bytes [128 t,
+            // 128 t + 128) in sub-tile t).
+            constexpr int kAC = Cfg::BK / 32;              // packed 16-byte chunks per row (8)
+            constexpr int kBPer = (BN / 4) * kAC / 32;     // W chunks per lane (4)
+            static_assert(Cfg::BK == 256 && BN == 64, "kTA layout");
+            const int q = warp - 8;
             int kb0, kb1;
             k_range(blockIdx.x, kb0, kb1);
-            for (int j = w; kb0 + j < kb1; j += 4) {
-                const uint32_t ph = (uint32_t)(j >> 2) & 1u;
-                const int sp = j % Cfg::SP;   // packed slot (slot sp is only ever used by warp sp % 4)
-                ptx::mbar_wait(&fullP[sp], (uint32_t)(j / Cfg::SP) & 1u);
-                ptx::mbar_wait(&empty8[w], ph ^ 1);
-                const uint8_t* src = ringP + sp * Cfg::kStageP;
-                uint8_t* dst = ring8 + w * Cfg::kStage8;
-                // Lane handles chunk c = lane & 3 of rows r0 + 8 i: the swizzle
-                // phase and both destination offsets are loop invariants.  All
-                // loads of a batch are issued before its stores (through generic
-                // pointers the compiler cannot hoist a load above a possibly
-                // aliasing store: one LDS -> STS round trip per chunk made a stage
-                // cost one warp ~1 us, tools/trace_small.py).
-                constexpr int kPer = kChunks / 32, kBatch = 12;
-                static_assert(kPer % kBatch == 0, "unpack batches");
-                const uint32_t r0 = (uint32_t)lane >> 2, c = (uint32_t)lane & 3u, r7 = r0 & 7u;
-                const uint32_t s0 = ptx::smem_u32(src) + r0 * 64u + c * 16u;
-                const uint32_t d0 = ptx::smem_u32(dst) + r0 * 128u;
-                const uint32_t dlo = ((2u * c) ^ r7) << 4, dhi = ((2u * c + 1u) ^ r7) << 4;
+            const int r = q * 32 + lane;
+            const uint32_t aoff = (uint32_t)r * 128u, af = (uint32_t)r & 7u;
+            const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+            for (int j = 0; kb0 + j < kb1; ++j) {
+                const int sp = j % SP, s8 = j % S8;
+                ptx::mbar_wait(&fullP[sp], (uint32_t)(j / SP) & 1u);
+                ptx::mbar_wait(&empty8[s8], ((uint32_t)(j / S8) & 1u) ^ 1u);
+                const uint32_t src = ptx::smem_u32(ringP + sp * Cfg::kStageP);
+                uint4 pa[kAC], pb[kBPer];
 #pragma unroll
-                for (int b = 0; b < kPer; b += kBatch) {
-                    uint4 pk[kBatch];
+                for (int c = 0; c < kAC; ++c) pa[c] = ptx::lds128(src + aoff + (((uint32_t)c ^ af) << 4));
 #pragma unroll
-                    for (int i = 0; i < kBatch; ++i) pk[i] = ptx::lds128(s0 + (uint32_t)(b + i) * 512u);
-#pragma unroll
-                    for (int i = 0; i < kBatch; ++i) {
-                        uint4 lo, hi;
-                        ptx::unpack_i4x8(pk[i].x, lo.x, hi.x);
-                        ptx::unpack_i4x8(pk[i].y, lo.y, hi.y);
-                        ptx::unpack_i4x8(pk[i].z, lo.z, hi.z);
-                        ptx::unpack_i4x8(pk[i].w, lo.w, hi.w);
-                        const uint32_t rb = d0 + (uint32_t)(b + i) * 1024u;
-                        ptx::sts128(rb + dlo, lo);
-                        ptx::sts128(rb + dhi, hi);
-                    }
+                for (int i = 0; i < kBPer; ++i) {
+                    const int id = lane + 32 * i;
+                    pb[i] = ptx::lds128(src + Cfg::kAP + (uint32_t)(16 * q + id / kAC) * 128u + (uint32_t)(id % kAC) * 16u);
                 }
-                ptx::fence_proxy_async_smem();
-                ptx::mbar_arrive(&full8[w]);
-                ptx::mbar_arrive(&emptyP[sp]);
+                const uint32_t tcol = tmem_base + lane_off + Cfg::kTaCol + Cfg::kTaStageCols * (uint32_t)s8;
+#pragma unroll
+                for (int hlf = 0; hlf < 2; ++hlf) {   // packed chunks 4 hlf .. 4 hlf + 3 -> 32 columns
+                    uint32_t w[32];
+#pragma unroll
+                    for (int cc = 0; cc < 4; ++cc) {
+                        const uint4 p = pa[4 * hlf + cc];
+                        ptx::unpack_i4x8(p.x, w[8 * cc + 0], w[8 * cc + 4]);
+                        ptx::unpack_i4x8(p.y, w[8 * cc + 1], w[8 * cc + 5]);
+                        ptx::unpack_i4x8(p.z, w[8 * cc + 2], w[8 * cc + 6]);
+                        ptx::unpack_i4x8(p.w, w[8 * cc + 3], w[8 * cc + 7]);
+                    }
+                    ptx::tmem_st_32x32b_x32(tcol + 32u * (uint32_t)hlf, w);
+                }
+                const uint32_t dst = ptx::smem_u32(ring8 + s8 * Cfg::kStage8 + Cfg::kA8);
+#pragma unroll
+                for (int i = 0; i < kBPer; ++i) {
+                    const int id = lane + 32 * i;
+                    const uint32_t rb = (uint32_t)(16 * q + id / kAC), cb = (uint32_t)(id % kAC);
+                    const uint32_t sub = dst + (cb >> 2) * (uint32_t)(BN * 128) + rb * 128u, cl = cb & 3u;
+                    uint4 lo, hi;
+                    ptx::unpack_i4x8(pb[i].x, lo.x, hi.x);
+                    ptx::unpack_i4x8(pb[i].y, lo.y, hi.y);
+                    ptx::unpack_i4x8(pb[i].z, lo.z, hi.z);
+                    ptx::unpack_i4x8(pb[i].w, lo.w, hi.w);
+                    ptx::sts128(sub + (((2u * cl) ^ (rb & 7u)) << 4), lo);
+                    ptx::sts128(sub + (((2u * cl + 1u) ^ (rb & 7u)) << 4), hi);
+                }
+                ptx::tmem_st_wait();             // this thread's A columns are written
+                ptx::fence_proxy_async_smem();   // and its W bytes visible to the tensor core
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    ptx::mbar_arrive(&full8[s8]);
+                    ptx::mbar_arrive(&emptyP[sp]);
+                }
             }
-            // tail: this slot's last MMA commit has landed
-            const int jl = (kb1 - kb0 - 1 - w) >= 0 ? ((kb1 - kb0 - 1 - w) / 4) * 4 + w : -1;
-            if (jl >= 0) ptx::mbar_wait(&empty8[w], (uint32_t)((jl >> 2) & 1));
+            // tail: the last MMA commit on slot q has landed
+            const int n = kb1 - kb0;
+            if (q < n) {
+                const int jl = ((n - 1 - q) / S8) * S8 + q;
+                ptx::mbar_wait(&empty8[q], (uint32_t)(jl / S8) & 1u);
+            }
         } else {
         int sp = 0, s8 = 0;
         uint32_t php = 0, ph8 = 0;
@@ -593,8 +636,9 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
         const int owned = ngroups > rank ? (ngroups - rank + splits - 1) / splits : 0;
         const int nwarps = (int)(blockDim.x >> 5);
         const uint32_t red0 = ptx::smem_u32(ring8);
-        static_assert(Cfg::BM * kRP <= 40960 && 40960 + (Cfg::kThreads / 32) * 4096 <= Cfg::S8 * Cfg::kStage8,
-                      "partials + per-warp staging fit the int8 ring");
+        static_assert(Cfg::BM * kRP <= 40960 &&
+                          40960 + (Cfg::kThreads / 32) * 4096 <= Cfg::S8 * Cfg::kStage8 + Cfg::SP * Cfg::kStageP,
+                      "partials + per-warp staging fit the idle rings (int8 ring, then the packed ring)");
         uint8_t* stage = ring8 + 40960 + warp * 4096;
         for (int u = warp; u < owned * kJ; u += nwarps) {
             const int grp = rank + splits * (u / kJ), j = u % kJ;

@@ -228,7 +228,8 @@ mkq_status launch_gemm(const void* a, int64_t lda, const void* w, int64_t ldw, i
     CUtensorMap ma, mb;
     const uint64_t kbytes = Cfg::kInt4 ? (uint64_t)K / 2 : (uint64_t)K;
     const uint32_t box_in = Cfg::kInt4 ? Cfg::BK / 2 : Cfg::BK;
-    mkq_status s = make_map(&ma, a, kbytes, (uint64_t)M, (uint64_t)lda, box_in, Cfg::BM, !Cfg::kInt4);
+    // kTA (small-M int4): packed 128-byte A rows with the 128-byte swizzle (conflict-free row reads by lane)
+    mkq_status s = make_map(&ma, a, kbytes, (uint64_t)M, (uint64_t)lda, box_in, Cfg::BM, !Cfg::kInt4 || Cfg::kTA);
     if (s != MKQ_OK) return s;
     s = make_map(&mb, w, kbytes, (uint64_t)N, (uint64_t)ldw, box_in, Cfg::BN, !Cfg::kInt4);
     if (s != MKQ_OK) return s;
