@@ -415,7 +415,7 @@ int small_m_mode() { return g_small_mode.load(std::memory_order_relaxed); }
 // Single wave only: 128 x 64 tiles if they fit one per SM, else the
 // large-tile paths.  K is split over a cluster while the clusters
 // still fit (one wave, <= 4 CTAs per cluster, >= 2 K-blocks per split).
-SmallPlan plan_small(int64_t M, int64_t N, int64_t K, int sms) {
+SmallPlan plan_small(int64_t M, int64_t N, int64_t K, int sms, bool int4) {
     SmallPlan p;
     const int mode = small_m_mode();
     if (mode == 0) return p;
@@ -431,7 +431,13 @@ SmallPlan plan_small(int64_t M, int64_t N, int64_t K, int sms) {
     p.use = true;
     const int64_t nk = (K + 127) / 128;
     int64_t sp = sms / std::max<int64_t>(p.tiles, 1);
-    sp = std::min<int64_t>(sp, nk / 2);   // >= 2 K-blocks per split
+    // K split only for long K: the cluster reduction (barrier + DSMEM round
+    // trip + a second store pass) costs more than it saves below 12 x 128 K
+    // per split for int4 (256-K stages), and always for int8 at Table-2 sizes
+    // (440 tokens: O 7.2 -> 5.3 us int4 / 6.5 -> 4.5 us int8 unsplit; FFN2
+    // int4 9.3 us split 2 vs 9.9 unsplit, int8 8.3 vs 7.9)
+    static const int min_kb = [] { const char* e = getenv("MKQ_SPLIT_MIN_KB"); return e ? atoi(e) : 12; }();
+    sp = int4 ? std::min<int64_t>(sp, nk / std::max(min_kb, 1)) : 1;
     static const int max_split = [] { const char* e = getenv("MKQ_MAX_SPLIT"); return e ? atoi(e) : 4; }();
     sp = std::min<int64_t>(sp, max_split);   // clusters of <= 4 full-SM CTAs co-reside in a GPC
     p.splits = (int)std::max<int64_t>(sp, 1);
@@ -520,7 +526,7 @@ mkq_status gemm_common(bool int4, const void* a, int64_t lda, const void* w, int
         if (e != cudaSuccess) return cuda_fail(e, "gemm_mma_small launch");
         return MKQ_OK;
     }
-    const SmallPlan sp = plan_small(M, N, K, sms);
+    const SmallPlan sp = plan_small(M, N, K, sms, int4);
     if (sp.use) {
         if (int4) return launch_gemm<mkq::GemmCfg<64, true>, true>(a, lda, w, ldw, (int)M, (int)N, (int)K, ep, sms, st, sp.splits);
         return launch_gemm<mkq::GemmCfg<64, false>, true>(a, lda, w, ldw, (int)M, (int)N, (int)K, ep, sms, st, sp.splits);
