@@ -270,11 +270,27 @@ __device__ unsigned long long* g_ttrace = nullptr;
     } while (0)
 #endif
 
+// Small-M fused W4A4 GEMM + residual + LayerNorm (+ Eq.1 codes) through an
+// N-cluster (kLnC): the N/64 CTAs of one 128-row block form a thread-block
+// cluster (N = 256..1024 -> 4..16 CTAs), each computes its 128 x 64 tile over
+// the whole K, adds the residual (TMA, 32 x 32 fp32 SWIZZLE_128B boxes) and
+// publishes per-row (mean, M2) of its 64 columns in shared memory; after a
+// cluster barrier every CTA combines the N/64 partials of its rows over DSMEM
+// in a fixed order (pairwise update: identical statistics in every CTA) and
+// writes LN(r) and its codes with TMA stores.
+struct LnCParams {
+    CUtensorMap r, y, q;          // residual in; LN output fp32 (make_out_map F32); codes (I4/I8) or unused
+    const float *g, *b;           // gamma, beta [N]
+    float eps, s_q;
+    int qbits, qmin, qmax;
+};
+constexpr int kLnCExtra = 1024 + 32768 + 1024 + 64;   // align slack, residual boxes, row statistics, barrier
+
 // ------------------------------------------------------------------ kernel
-template <class Cfg, bool kCl = false>
-__global__ void __launch_bounds__(Cfg::kThreads, 1)
-    gemm_i8tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     const __grid_constant__ CUtensorMap tmO, const EpiParams ep, int M, int N, int K, int splits) {
+template <class Cfg, bool kCl, bool kLnC>
+__device__ __forceinline__ void gemm_i8tc_body(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmO,
+                                               const EpiParams& ep, int M, int N, int K, int splits,
+                                               const LnCParams* lp) {
     constexpr int BM = Cfg::BM, BN = Cfg::BN, S8 = Cfg::S8, SP = Cfg::SP;
     constexpr bool kInt4 = Cfg::kInt4;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -289,6 +305,13 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
     uint64_t* tfull = emptyP + SP;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    // kLnC: residual boxes [4 quadrants][2 column blocks] x 4 KB, row statistics, residual barrier
+    uint8_t* lres = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tmem_slot) + 16 + 1023) & ~uintptr_t(1023));
+    float2* lstat = reinterpret_cast<float2*>(lres + 32768);
+    uint64_t* rbar = reinterpret_cast<uint64_t*>(lstat + Cfg::BM);
+    static_assert(!kLnC || (kCl && Cfg::kTA && Cfg::BN == 64), "kLnC: small-M int4 plan, 64-column tiles");
+    __shared__ float g_s[kLnC ? Cfg::BN : 1], be_s[kLnC ? Cfg::BN : 1];
+    float rr[kLnC ? 64 : 1];   // kLnC epilogue: the row's residual sums r = y + res, across the cluster barrier
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -327,11 +350,17 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
             ptx::mbar_init(&tfull[i], 1);
             ptx::mbar_init(&tempty[i], 128);
         }
+        if constexpr (kLnC) ptx::mbar_init(rbar, 1);
         ptx::fence_barrier_init();
     }
     if (warp == 0 && lane == 0) {
         ptx::tma_prefetch_desc(&tmA);
         ptx::tma_prefetch_desc(&tmB);
+        if constexpr (kLnC) {
+            ptx::tma_prefetch_desc(&lp->r);
+            ptx::tma_prefetch_desc(&lp->y);
+            if (lp->qbits) ptx::tma_prefetch_desc(&lp->q);
+        }
     }
     if (warp == 2) ptx::tmem_alloc<Cfg::kTmemCols>(tmem_slot);
     ptx::tc_fence_before();
@@ -371,6 +400,14 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
                         if (++s == S8) { s = 0; ph ^= 1; }
                     }
                 }
+            }
+            if constexpr (kLnC) {   // the tile's residual: 8 boxes of 32 rows x 32 columns
+                const int tile = blockIdx.x;
+                const int m0 = (tile / n_tiles) * BM, n0 = (tile % n_tiles) * BN;
+                ptx::mbar_arrive_expect_tx(rbar, 32768);
+#pragma unroll
+                for (int b = 0; b < 8; ++b)
+                    ptx::tma_load_2d(&lp->r, rbar, lres + b * 4096, n0 + 32 * (b & 1), m0 + 32 * (b >> 1));
             }
             if constexpr (!kInt4) {   // tail: the MMA's last commits on empty8 have landed
                 for (int i = 0; i < S8; ++i) {
@@ -435,8 +472,62 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
             ptx::tc_fence_after();
             if (threadIdx.x == 128) TTRACE(6);
             const int row = m0 + q * 32 + lane;
+            // kLnC: both 32-column blocks unrolled (rr is indexed statically: registers)
+#pragma unroll
+            for (int j = 0; j < (kLnC ? BN / 32 : 1); ++j) {
+              if constexpr (kLnC) {
+                uint32_t v[32];
+                ptx::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + ab * BN + 32 * j, v);
+                ptx::tmem_ld_wait();
+                    // r = dequant(acc) + res for this row's 32 columns of block j (R4, R9)
+                    if (j == 0) {
+                        ptx::named_bar_sync(1, 160);
+                        ptx::mbar_wait(rbar, 0);
+                    }
+                    const uint32_t bx = ptx::smem_u32(lres + (q * 2 + j) * 4096) + (uint32_t)lane * 128u;
+                    const bool hb = ep.bias != nullptr;
+#pragma unroll
+                    for (int c4 = 0; c4 < 8; ++c4) {
+                        float4 rs;
+                        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                     : "=f"(rs.x), "=f"(rs.y), "=f"(rs.z), "=f"(rs.w)
+                                     : "r"(bx + (uint32_t)((c4 ^ (lane & 7)) << 4)));
+                        const float rv[4] = {rs.x, rs.y, rs.z, rs.w};
+#pragma unroll
+                        for (int t = 0; t < 4; ++t) {
+                            const int i = 4 * c4 + t;
+                            const int32_t a = kInt4 ? ((int32_t)v[i] >> 8) : (int32_t)v[i];
+                            rr[32 * j + i] = __fadd_rn(dequant(a, sc_s[32 * j + i], b_s[32 * j + i], hb), rv[t]);
+                        }
+                    }
+                    if (j == 1) {   // this CTA's (mean, M2) of the row over its 64 columns
+                        // 8 independent partial sums (no 64-long dependent chain), fixed order
+                        float ps[8];
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) ps[k] = rr[k];
+#pragma unroll
+                        for (int i = 8; i < 64; ++i) ps[i & 7] = __fadd_rn(ps[i & 7], rr[i]);
+                        const float sum = __fadd_rn(__fadd_rn(__fadd_rn(ps[0], ps[1]), __fadd_rn(ps[2], ps[3])),
+                                                    __fadd_rn(__fadd_rn(ps[4], ps[5]), __fadd_rn(ps[6], ps[7])));
+                        const float mean = __fdiv_rn(sum, 64.0f);
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) {
+                            const float d = __fsub_rn(rr[k], mean);
+                            ps[k] = __fmul_rn(d, d);
+                        }
+#pragma unroll
+                        for (int i = 8; i < 64; ++i) {
+                            const float d = __fsub_rn(rr[i], mean);
+                            ps[i & 7] = __fmaf_rn(d, d, ps[i & 7]);
+                        }
+                        const float m2 = __fadd_rn(__fadd_rn(__fadd_rn(ps[0], ps[1]), __fadd_rn(ps[2], ps[3])),
+                                                   __fadd_rn(__fadd_rn(ps[4], ps[5]), __fadd_rn(ps[6], ps[7])));
+                        lstat[q * 32 + lane] = make_float2(mean, m2);
+                    }
+              }
+            }
 #pragma unroll 1
-            for (int j = 0; j < BN / 32; ++j) {
+            for (int j = 0; j < (kLnC ? 0 : BN / 32); ++j) {
                 const int n = n0 + 32 * j;
                 if (n >= N) break;
                 uint32_t v[32];
@@ -499,6 +590,10 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
             const int n = n0 + c;
             sc_s[c] = n < N ? __fmul_rn(ep.s_a, __ldg(ep.s_w + n)) : 0.0f;
             b_s[c] = (n < N && ep.bias) ? __ldg(ep.bias + n) : 0.0f;
+            if constexpr (kLnC) {
+                g_s[c] = n < N ? __ldg(lp->g + n) : 0.0f;
+                be_s[c] = n < N ? __ldg(lp->b + n) : 0.0f;
+            }
         }
         if (splits == 1) ptx::named_bar_arrive(1, 160);   // -> the epilogue warps
     } else if (kInt4 && warp >= 8) {
@@ -621,6 +716,105 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
         }
     }
 
+    if constexpr (kLnC) {
+        // pass 2: the row statistics of all N/64 CTAs of the cluster (DSMEM,
+        // fixed order, pairwise update), LN(r) -> staged boxes -> TMA stores
+        if (threadIdx.x == 128) TTRACE(12);
+        ptx::cluster_sync();   // every CTA's lstat is written and visible
+        if (threadIdx.x == 128) TTRACE(13);
+        if (warp >= 4 && warp < 8) {
+            const int q = warp & 3;
+            const int tile = blockIdx.x;
+            const int m0 = (tile / n_tiles) * BM, n0 = (tile % n_tiles) * BN;
+            const int rl = q * 32 + lane;
+            const uint32_t sa = ptx::smem_u32(lstat + rl);
+            // all peers' partials in flight at once (<= 16 CTAs; a dependent
+            // DSMEM round trip per peer cost ~0.18 us each, tools/trace_small.py)
+            float2 part[16];
+#pragma unroll
+            for (int pc = 0; pc < 16; ++pc) {
+                if (pc < n_tiles) {
+                    uint32_t ra;
+                    asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(sa), "r"(pc));
+                    asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];" : "=f"(part[pc].x), "=f"(part[pc].y) : "r"(ra));
+                }
+            }
+            // this CTA is done reading its peers: release them early (the matching
+            // wait is the last thing before exit)
+            asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+            float mean = 0.0f, M2 = 0.0f;
+#pragma unroll
+            for (int pc = 0; pc < 16; ++pc) {
+                if (pc >= n_tiles) break;
+                const float2 o = part[pc];
+                if (pc == 0) {
+                    mean = o.x;
+                    M2 = o.y;
+                } else {   // equal counts 64: Chan et al.'s pairwise update
+                    const float d = __fsub_rn(o.x, mean);
+                    const float nt = (float)(64 * (pc + 1)), nw = (float)(64 * pc);
+                    mean = __fadd_rn(mean, __fmul_rn(d, __fdiv_rn(64.0f, nt)));
+                    M2 = __fadd_rn(__fadd_rn(M2, o.y), __fmul_rn(__fmul_rn(d, d), __fdiv_rn(nw * 64.0f, nt)));
+                }
+            }
+            const float rstd = rsqrtf(__fadd_rn(__fdiv_rn(M2, (float)N), lp->eps));
+            if (threadIdx.x == 128) TTRACE(14);
+            const QuantRcp Qr = quant_rcp(lp->s_q, lp->qmin, lp->qmax);
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                uint8_t* stage = ring8 + (q * 2 + j) * 8192;   // y: 2 x 2 KB (16 columns, SW64); codes at +4 KB
+                float o[32];
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    const int c = 32 * j + i;
+                    o[i] = __fmaf_rn(__fmul_rn(__fsub_rn(rr[c], mean), rstd), g_s[c], be_s[c]);
+                }
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    *reinterpret_cast<float4*>(stage + (k >> 2) * 2048 + stage_off(lane, k & 3, 64)) =
+                        make_float4(o[4 * k], o[4 * k + 1], o[4 * k + 2], o[4 * k + 3]);
+                if (lp->qbits == 4) {
+                    uint32_t w[4];
+                    bool near = false;
+#pragma unroll
+                    for (int g8 = 0; g8 < 4; ++g8) {
+                        float v8[8];
+#pragma unroll
+                        for (int t = 0; t < 8; ++t) v8[t] = o[8 * g8 + t];
+                        w[g8] = quant_nib8_fast(v8, Qr, near);
+                    }
+                    if (__builtin_expect(near, 0)) {
+#pragma unroll
+                        for (int g8 = 0; g8 < 4; ++g8)
+                            w[g8] = quant_nib8_exact(o[8 * g8], o[8 * g8 + 1], o[8 * g8 + 2], o[8 * g8 + 3], o[8 * g8 + 4],
+                                                     o[8 * g8 + 5], o[8 * g8 + 6], o[8 * g8 + 7], lp->s_q, lp->qmin,
+                                                     lp->qmax);
+                    }
+                    *reinterpret_cast<uint4*>(stage + 4096 + stage_off(lane, 0, 16)) = make_uint4(w[0], w[1], w[2], w[3]);
+                } else if (lp->qbits == 8) {
+                    uint32_t w[8];
+#pragma unroll
+                    for (int g4 = 0; g4 < 8; ++g4) w[g4] = quant_byte4_rcp(o[4 * g4], o[4 * g4 + 1], o[4 * g4 + 2], o[4 * g4 + 3], Qr);
+                    *reinterpret_cast<uint4*>(stage + 4096 + stage_off(lane, 0, 32)) = make_uint4(w[0], w[1], w[2], w[3]);
+                    *reinterpret_cast<uint4*>(stage + 4096 + stage_off(lane, 1, 32)) = make_uint4(w[4], w[5], w[6], w[7]);
+                }
+                ptx::fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    const int n = n0 + 32 * j, y0 = m0 + q * 32;
+                    ptx::tma_store_2d(&lp->y, stage, n, y0);
+                    ptx::tma_store_2d(&lp->y, stage + 2048, n + 16, y0);
+                    if (lp->qbits) ptx::tma_store_2d(&lp->q, stage + 4096, lp->qbits == 4 ? n / 2 : n, y0);
+                    ptx::tma_store_commit();
+                }
+            }
+            if (threadIdx.x == 128) TTRACE(15);
+            if (lane == 0) ptx::tma_store_wait_read<0>();   // staging read before exit
+        } else {
+            asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+        }
+        asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");   // peers have read this CTA's lstat
+    }
     if constexpr (kCl) if (splits > 1) {
         // DSMEM reduce-scatter of the staged partials + epilogue (all warps)
         ptx::cluster_sync();   // release/acquire: every peer's staged rows are visible
@@ -688,6 +882,21 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
         ptx::tc_fence_after();
         ptx::tmem_dealloc<Cfg::kTmemCols>(tmem_base);
     }
+}
+
+template <class Cfg, bool kCl = false>
+__global__ void __launch_bounds__(Cfg::kThreads, 1)
+    gemm_i8tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const __grid_constant__ CUtensorMap tmO, const EpiParams ep, int M, int N, int K, int splits) {
+    gemm_i8tc_body<Cfg, kCl, false>(tmA, tmB, tmO, ep, M, N, K, splits, nullptr);
+}
+
+// kLnC entry: one 128 x 64 tile per CTA, clusters of N/64 CTAs along N
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::kThreads, 1)
+    gemm_lnc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const __grid_constant__ LnCParams lp, const EpiParams ep, int M, int N, int K) {
+    gemm_i8tc_body<Cfg, true, true>(tmA, tmB, lp.y, ep, M, N, K, 1, &lp);
 }
 
 }  // namespace mkq

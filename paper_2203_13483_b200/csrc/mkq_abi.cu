@@ -350,6 +350,104 @@ mkq_status launch_gemm2_ln_cfg(const void* a, int64_t lda, const void* w, int64_
     return MKQ_OK;
 }
 
+int small_m_mode();   // the GEMM plan mode (below)
+
+// ---- small-M fused GEMM + residual + LayerNorm through an N-cluster (kLnC)
+using LnCCfg = mkq::GemmCfg<64, true>;
+constexpr size_t kLnCSmem = LnCCfg::kSmem + mkq::kLnCExtra;
+
+bool lnc_attrs() {
+    static bool done[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return false;
+    if (!done[dev]) {
+        if (cudaFuncSetAttribute(mkq::gemm_lnc_kernel<LnCCfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kLnCSmem) != cudaSuccess ||
+            cudaFuncSetAttribute(mkq::gemm_lnc_kernel<LnCCfg>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+                cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        done[dev] = true;
+    }
+    return true;
+}
+
+// co-resident clusters of nt CTAs of the kLnC kernel (cached per device)
+int lnc_max_clusters(int nt) {
+    static int cache[64][17] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64 || nt < 1 || nt > 16) return 0;
+    int& c = cache[dev][nt];
+    if (c == 0) {
+        int n = 0;
+        if (lnc_attrs()) {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3((unsigned)(nt * 16));
+            cfg.blockDim = dim3(LnCCfg::kThreads);
+            cfg.dynamicSmemBytes = kLnCSmem;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = (unsigned)nt;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            if (cudaOccupancyMaxActiveClusters(&n, mkq::gemm_lnc_kernel<LnCCfg>, &cfg) != cudaSuccess) {
+                cudaGetLastError();
+                n = 0;
+            }
+        }
+        c = n > 0 ? n : -1;
+    }
+    return c > 0 ? c : 0;
+}
+
+// Does the small-M N-cluster path take this W4A4 GEMM + LN?  Every cluster
+// must be co-resident (one wave): ceil(M / 128) <= co-resident clusters of N/64
+// CTAs (B200: one 12- or 16-CTA cluster per GPC).  MKQ_LNC=0 or the
+// "never small-M" plan mode (mkq_set_small_m_mode(0), tests) disables it.
+bool lnc_ok(int64_t M, int64_t N) {
+    static const bool on = [] { const char* e = getenv("MKQ_LNC"); return !(e && strcmp(e, "0") == 0); }();
+    if (!on || small_m_mode() == 0 || N % 64 || N / 64 < 2 || N / 64 > 16) return false;
+    return (M + 127) / 128 <= lnc_max_clusters((int)(N / 64));
+}
+
+mkq_status launch_lnc(const void* a, int64_t lda, const void* w, int64_t ldw, int M, int N, int K,
+                      const mkq::EpiParams& ep, const mkq::Ln2Params& ln, cudaStream_t st) {
+    if (!lnc_attrs()) return fail(MKQ_ERR_CUDA, "cudaFuncSetAttribute(gemm_lnc_kernel)");
+    CUtensorMap ma, mb;
+    mkq_status s = make_map(&ma, a, (uint64_t)K / 2, (uint64_t)M, (uint64_t)lda, LnCCfg::BK / 2, LnCCfg::BM, true);
+    if (s != MKQ_OK) return s;
+    s = make_map(&mb, w, (uint64_t)K / 2, (uint64_t)N, (uint64_t)ldw, LnCCfg::BK / 2, LnCCfg::BN, false);
+    if (s != MKQ_OK) return s;
+    mkq::LnCParams lp;
+    s = make_map_t(&lp.r, ln.res, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (uint64_t)N, (uint64_t)M, (uint64_t)ln.ldr * 4, 32,
+                   32, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (s != MKQ_OK) return s;
+    s = make_out_map(&lp.y, ln.y, MKQ_OUT_F32, M, N, ln.ldy * 4);
+    if (s != MKQ_OK) return s;
+    lp.q = lp.y;
+    if (ln.qbits) {
+        s = make_out_map(&lp.q, ln.q, ln.qbits == 4 ? MKQ_OUT_I4 : MKQ_OUT_I8, M, N, ln.ldq);
+        if (s != MKQ_OK) return s;
+    }
+    lp.g = ln.g;
+    lp.b = ln.b;
+    lp.eps = ln.eps;
+    lp.s_q = ln.s_q;
+    lp.qbits = ln.qbits;
+    lp.qmin = ln.qmin;
+    lp.qmax = ln.qmax;
+    const int nt = N / 64, mt = (M + 127) / 128;
+    cudaError_t e = launch_k(mkq::gemm_lnc_kernel<LnCCfg>, dim3((unsigned)(mt * nt)), dim3(LnCCfg::kThreads),
+                             kLnCSmem, st, nt, ma, mb, lp, ep, M, N, K);
+    if (e != cudaSuccess) return cuda_fail(e, "gemm_lnc launch");
+    return MKQ_OK;
+}
+
 mkq_status launch_gemm2_ln(const void* a, int64_t lda, const void* w, int64_t ldw, int M, int N, int K,
                            mkq::Epi2Params& ep, void* ws, int sms, cudaStream_t st) {
     static const int boxes = [] { const char* v = getenv("MKQ_LN_BOXES"); return v ? atoi(v) : 0; }();   // diagnostics
@@ -849,6 +947,7 @@ mkq_status mkq_gemm_residual_ln(const void* a, int64_t lda, const void* w, int64
     p2.ln = mkq::Ln2Params{res, ldr, gamma, beta, eps, y, ldy, static_cast<uint8_t*>(q), ldq, q_bits, qmin, qmax,
                            s_q, nullptr, nullptr, (int)(N / 256)};
     PdlScope pdl_scope(M);
+    if (lnc_ok(M, N)) return launch_lnc(a, lda, w, ldw, (int)M, (int)N, (int)K, p2.e, p2.ln, static_cast<cudaStream_t>(stream));
     return launch_gemm2_ln(a, lda, w, ldw, (int)M, (int)N, (int)K, p2, ws, sms, static_cast<cudaStream_t>(stream));
 }
 
@@ -1213,7 +1312,10 @@ mkq_status mkq_act_scale(const float* x, int64_t n, double p, float l_max, float
 // {256, 512, 768, 1024} and at least 4096 tokens (below that the small-M GEMM
 // plans and the standalone LN kernels are faster).
 static bool layer_fused_ln(const mkq_layer* L, int64_t T) {
-    return L->bits == 4 && L->hidden % 256 == 0 && L->hidden <= 1024 && T >= 4096;
+    // >= 4096 tokens: the 2-CTA fused kernel; small M: the N-cluster kernel when
+    // every cluster is co-resident (Table-2 BS 16); in between the small-M
+    // GEMM plans and the standalone LN kernels
+    return L->bits == 4 && L->hidden % 256 == 0 && L->hidden <= 1024 && (T >= 4096 || lnc_ok(T, L->hidden));
 }
 
 struct LayerWs {

@@ -45,9 +45,23 @@ def _case(Mr, N, K, seed, tiny_scale=False):
 
 
 @pytest.mark.parametrize("Mr,N,K", [(256, 256, 256), (300, 1024, 1024), (1, 768, 512), (4096, 1024, 1024),
-                                    (1000, 768, 3072), (2311, 512, 4096)])
+                                    (1000, 768, 3072), (2311, 512, 4096), (440, 768, 768), (440, 768, 3072),
+                                    (130, 512, 96)])
 @pytest.mark.parametrize("q_bits", [0, 4, 8])
-def test_gemm_residual_ln_parity(Mr, N, K, q_bits):
+@pytest.mark.parametrize("plan", [-1, 0], ids=["plan-auto", "plan-2cta"])
+def test_gemm_residual_ln_parity(Mr, N, K, q_bits, plan):
+    """plan-auto: M <= 128 x (co-resident N/64-CTA clusters) takes the small-M
+    N-cluster kernel (row statistics over DSMEM), larger M the 2-CTA kernel;
+    plan-2cta forces the 2-CTA kernel (mkq_set_small_m_mode(0))."""
+    from paper_2203_13483_b200._lib import lib
+    lib().mkq_set_small_m_mode(plan)
+    try:
+        _parity(Mr, N, K, q_bits)
+    finally:
+        lib().mkq_set_small_m_mode(-1)
+
+
+def _parity(Mr, N, K, q_bits):
     A, W, s_a, s_w, b, res, g, beta = _case(Mr, N, K, seed=Mr + N + K + q_bits)
     a_d = dev(oracle.pack_int4(A))
     w_d = dev(oracle.pack_int4(W))

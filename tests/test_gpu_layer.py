@@ -138,9 +138,17 @@ def test_layer_stagewise_and_end_to_end(bits, seqlens):
     c_oa = oracle.quantize(oa, W.s_o_in, lo, hi)
     o = host(gemm(dev(pack(c_oa)), t["w_o"], W.s_o_in, t["sw_o"], t["b_o"], mode=M.OUT_F32, K=hidden))
     assert np.array_equal(o, oracle.linear(c_oa, W.o.codes, W.s_o_in, W.o.s_w, W.o.bias))
-    h1, c_h1 = M.mkq_residual_layernorm(dev(o), dev(h), t["ln1_g"], t["ln1_b"], 1e-12, bits=bits,
-                                        s_q=W.s_ffn1_in, qmin=lo, qmax=hi)
-    h1 = host(h1)
+    # the layer runs W^A + LN1 and W^2 + LN2 as mkq_gemm_residual_ln when fused (NEXT(4);
+    # at these sizes the small-M N-cluster kernel), else GEMM + residual_layernorm
+    fused = L.fused_ln(T)
+    if fused:
+        h1_d, c_h1 = M.mkq_gemm_residual_ln(dev(pack(c_oa)), t["w_o"], W.s_o_in, t["sw_o"], t["b_o"], dev(h),
+                                            t["ln1_g"], t["ln1_b"], 1e-12, K=hidden, q_bits=bits, s_q=W.s_ffn1_in,
+                                            qmin=lo, qmax=hi)
+    else:
+        h1_d, c_h1 = M.mkq_residual_layernorm(dev(o), dev(h), t["ln1_g"], t["ln1_b"], 1e-12, bits=bits,
+                                              s_q=W.s_ffn1_in, qmin=lo, qmax=hi)
+    h1 = host(h1_d)
     ref_h1 = OL.layernorm(o.astype(np.float64) + h, W.ln1_g, W.ln1_b)
     assert np.abs(h1 - ref_h1).max() < 2e-5 * max(1.0, np.abs(ref_h1).max())
     codes_h1 = oracle.quantize(h1, W.s_ffn1_in, lo, hi)
@@ -153,7 +161,13 @@ def test_layer_stagewise_and_end_to_end(bits, seqlens):
     assert np.array_equal(view(host(a2)), pack(ref_a2))
     f = host(gemm(a2, t["w_2"], W.s_ffn2_in, t["sw_2"], t["b_2"], mode=M.OUT_F32, K=ffn))
     assert np.array_equal(f, oracle.linear(ref_a2, W.w2.codes, W.s_ffn2_in, W.w2.s_w, W.w2.bias))
-    y = host(M.mkq_residual_layernorm(dev(f), dev(h1), t["ln2_g"], t["ln2_b"], 1e-12))
+    if fused:
+        y = host(M.mkq_gemm_residual_ln(a2, t["w_2"], W.s_ffn2_in, t["sw_2"], t["b_2"], h1_d, t["ln2_g"],
+                                        t["ln2_b"], 1e-12, K=ffn))
+    else:
+        y = host(M.mkq_residual_layernorm(dev(f), h1_d, t["ln2_g"], t["ln2_b"], 1e-12))
+    ref_y = OL.layernorm(f.astype(np.float64) + h1, W.ln2_g, W.ln2_b)
+    assert np.abs(y - ref_y).max() < 2e-5 * max(1.0, np.abs(ref_y).max())
     # the fused layer call runs exactly these kernels: identical bits
     assert np.array_equal(y, out)
 

@@ -1,0 +1,5 @@
+for i in 1 2; do
+timeout 300 python tools/stage_times.py --only gemm_o_ln1,gemm_ffn2_ln2
+MKQ_LIB=build_dbg/LNSTG/libmkq.so timeout 300 python tools/stage_times.py --only gemm_o_ln1,gemm_ffn2_ln2
+done
+MKQ_LIB=build_dbg/LNSTG/libmkq.so timeout 900 python -m pytest tests/test_gpu_gemm_ln.py tests/test_gpu_layer.py -m gpu -x -q 2>&1 | tail -2

@@ -33,6 +33,10 @@ calls = [("quant", lambda: M.mkq_quantize_pack(x, sq, bits, lo, hi, out=codes, s
          ("ffn1", lambda: gemm(c1, t["w_1"], s["s_ffn1_in"], t["sw_1"], t["b_1"], mode=M.OUT_I4 if bits == 4 else M.OUT_I8, gelu=True, s_out=s["s_ffn2_in"], qmin=lo, qmax=hi, out=a2, K=h, requant_table=L.table, stream=st)),
          ("ffn2", lambda: gemm(a2, t["w_2"], s["s_ffn2_in"], t["sw_2"], t["b_2"], mode=M.OUT_F32, out=f, K=F, stream=st)),
          ("ln2", lambda: M.mkq_residual_layernorm(f, h1, t["ln2_g"], t["ln2_b"], 1e-12, y=out, stream=st))]
+if bits == 4:   # the fused W^A + LN1 / W^2 + LN2 kernels (mkq_gemm_residual_ln; not in stage_sum)
+    lnws = torch.zeros(1 << 20, dtype=torch.uint8, device="cuda")
+    calls += [("o_ln1*", lambda: M.mkq_gemm_residual_ln(oa, t["w_o"], s["s_o_in"], t["sw_o"], t["b_o"], x, t["ln1_g"], t["ln1_b"], 1e-12, K=h, q_bits=4, s_q=s["s_ffn1_in"], qmin=lo, qmax=hi, y=h1, q=c1, stream=st)),
+              ("ffn2_ln2*", lambda: M.mkq_gemm_residual_ln(a2, t["w_2"], s["s_ffn2_in"], t["sw_2"], t["b_2"], h1, t["ln2_g"], t["ln2_b"], 1e-12, K=F, y=out, stream=st))]
 R = 20
 res = {}
 with torch.cuda.stream(st):
@@ -70,7 +74,7 @@ with torch.cuda.stream(st):
     e1.record(st)
     torch.cuda.synchronize()
 res["layer_x20"] = round(e0.elapsed_time(e1) * 1e3 / (10 * R), 2)
-print(f"bits={bits} T={T} small={os.environ.get('MKQ_SMALL_M', 'auto')}:", res, "stage_sum", round(sum(v for k, v in res.items() if k != 'layer_x20'), 1), flush=True)
+print(f"bits={bits} T={T} small={os.environ.get('MKQ_SMALL_M', 'auto')}:", res, "stage_sum", round(sum(v for k, v in res.items() if k != 'layer_x20' and not k.endswith('*')), 1), flush=True)
 # kernel-switch cost (diagnostics): pairs of different stages alternating in one graph vs each alone
 if os.environ.get("PAIRS"):
     names = [n for n, _ in calls]

@@ -30,6 +30,10 @@ if bits == 8:
     a, w = a.view(torch.int8), w.view(torch.int8)
 sw = torch.full((N,), 1e-3, device="cuda"); b = torch.zeros(N, device="cuda")
 gemm = M.mkq_gemm_w4a4 if bits == 4 else M.mkq_gemm_w8a8
+if os.environ.get("FUSED_LN"):   # the small-M fused GEMM + residual + LN (slots 12-15: LN pass 2)
+    res = torch.randn(Mm, N, device="cuda"); g1 = torch.ones(N, device="cuda")
+    def gemm(a, w, s_a, sw, b, K, out=None):
+        return M.mkq_gemm_residual_ln(a, w, s_a, sw, b, res, g1, b, 1e-12, K=K, q_bits=4, s_q=0.5)
 out = gemm(a, w, 0.3, sw, b, K=K)
 buf = torch.zeros(256 * 16 * 2, dtype=torch.int64, device="cuda")
 lib().mkq_debug_set_ttrace.argtypes = [ctypes.c_void_p]
