@@ -179,7 +179,11 @@ MKQ_API size_t mkq_gemm_workspace_size(int64_t M, int64_t N, int64_t K);
  * summation order: results agree with mkq_gemm_w4a4 + mkq_residual_layernorm
  * within LN rounding, and are deterministic).  ws >=
  * mkq_gemm_residual_ln_workspace_size(M, N) bytes (row-statistics exchange
- * between the CTAs of a row; the call zeroes its counters on `stream`). */
+ * between the CTAs of a row; the call zeroes its counters on `stream`).
+ * Two kernels, same contract: for small M (ceil(M/128) co-resident clusters of
+ * N/64 CTAs, e.g. the paper's Table-2 batches) one thread-block cluster per
+ * 128-row block exchanges the row statistics over distributed shared memory
+ * and does not touch ws; otherwise CTA pairs exchange them through ws. */
 MKQ_API size_t mkq_gemm_residual_ln_workspace_size(int64_t M, int64_t N);
 MKQ_API mkq_status mkq_gemm_residual_ln(const void *a, int64_t lda_bytes, const void *w, int64_t ldw_bytes,
                                         int64_t M, int64_t N, int64_t K, float s_a, const float *s_w,
