@@ -46,14 +46,25 @@ def part_gemm():
         M.mkq_gemm_w4a4(rnd_u8(130, 256), W, 0.3, sw[:512], b[:512], mode=M.OUT_F32, K=512)
         M.mkq_gemm_w4a4(rnd_u8(130, 1536), rnd_u8(256, 1536), 0.3, sw[:256], b[:256], mode=M.OUT_I4, gelu=True,
                         s_out=0.05, K=3072)
+        # small-M plan, unsplit: A in TMEM, TMA-stored epilogue (fp16 out, the QKV shape class)
+        M.mkq_gemm_w4a4(rnd_u8(200, 384), rnd_u8(256, 384), 0.3, sw[:256], b[:256], mode=M.OUT_F16, K=768)
     lib().mkq_set_small_m_mode(-1)
-    # fused GEMM + residual + LN (+ codes), N = 768 (three CTA pairs per row group)
+    # Table-2 FFN1: GELU + int4 requant through the compact table on 256 x 128 CTA-pair tiles
+    sw3 = torch.rand(3072, device=dev, generator=g) * 1e-3 + 1e-4
+    b3 = torch.rand(3072, device=dev, generator=g) * 0.1
+    M.mkq_gemm_w4a4(rnd_u8(440, 384), rnd_u8(3072, 384), 0.3, sw3, b3, mode=M.OUT_I4, gelu=True, s_out=0.05, K=768,
+                    requant_table=True)
+    # fused GEMM + residual + LN (+ codes), N = 768: the small-M N-cluster kernel (auto at
+    # M = 300) and the 2-CTA kernel (three CTA pairs per row group; plan mode 0)
     res = torch.randn(300, 768, device=dev, generator=g)
     one, zero = torch.ones(768, device=dev), torch.zeros(768, device=dev)
-    for qb in (0, 4, 8):
-        M.mkq_gemm_residual_ln(rnd_u8(300, 256), rnd_u8(768, 256), 0.3, sw[:768], b[:768], res, one, zero, 1e-12,
-                               K=512, q_bits=qb, s_q=0.5 if qb == 4 else 0.02, qmin=-8 if qb != 8 else -128,
-                               qmax=7 if qb != 8 else 127)
+    for plan in (-1, 0):
+        lib().mkq_set_small_m_mode(plan)
+        for qb in (0, 4, 8):
+            M.mkq_gemm_residual_ln(rnd_u8(300, 256), rnd_u8(768, 256), 0.3, sw[:768], b[:768], res, one, zero, 1e-12,
+                                   K=512, q_bits=qb, s_q=0.5 if qb == 4 else 0.02, qmin=-8 if qb != 8 else -128,
+                                   qmax=7 if qb != 8 else 127)
+    lib().mkq_set_small_m_mode(-1)
 
 
 def part_attn():
