@@ -339,12 +339,12 @@ __device__ __forceinline__ void gemm_i8tc_body(const CUtensorMap& tmA, const CUt
     static_assert(!Cfg::kTA || kCl, "A in TMEM: one tile per CTA (small-M plan)");
     if (threadIdx.x == 0) {
         for (int i = 0; i < S8; ++i) {
-            ptx::mbar_init(&full8[i], Cfg::kTA ? 4 : (kInt4 ? (kCl ? 32 : 128) : 1));
+            ptx::mbar_init(&full8[i], Cfg::kTA ? 8 : (kInt4 ? (kCl ? 32 : 128) : 1));
             ptx::mbar_init(&empty8[i], 1);
         }
         for (int i = 0; i < SP; ++i) {
             ptx::mbar_init(&fullP[i], 1);
-            ptx::mbar_init(&emptyP[i], Cfg::kTA ? 4 : (kCl ? 32 : 128));
+            ptx::mbar_init(&emptyP[i], Cfg::kTA ? 8 : (kCl ? 32 : 128));
         }
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(&tfull[i], 1);
@@ -370,6 +370,76 @@ __device__ __forceinline__ void gemm_i8tc_body(const CUtensorMap& tmA, const CUt
     ptx::pdl_launch();
     ptx::pdl_wait();
     if (threadIdx.x == 0) TTRACE(1);
+
+    // Small-M plan, A in TMEM (kTA): the stage's unpack is split between two
+    // warps per TMEM lane quadrant q (the unpack warp 8+q, half 0, and the
+    // epilogue warp 4+q, half 1, which is idle until the accumulator is ready;
+    // one warp per quadrant left a 256-K stage ~0.5 us of unpack latency).
+    // Half h expands packed A chunks 4h..4h+3 of row 32q + lane (lane = row;
+    // packed A arrives with the TMA 128-byte swizzle, so the lanes' row reads
+    // are conflict-free) into TMEM columns 32h..32h+31 of the stage with one
+    // tcgen05.st (column 8c..8c+3 = even codes of packed chunk c, 8c+4..8c+7 =
+    // odd codes: the permutation W gets in shared memory), and W chunks 2h,
+    // 2h+1 of each lane (rows 16q..16q+15) into the SW128 sub-tiles (K bytes
+    // [128 t, 128 t + 128) in sub-tile t).
+    auto ta_unpack = [&](int q, int h) {
+        if constexpr (Cfg::kTA) {
+            constexpr int kAC = Cfg::BK / 32;              // packed 16-byte chunks per row (8)
+            constexpr int kBPer = (BN / 4) * kAC / 32;     // W chunks per lane (4)
+            static_assert(Cfg::BK == 256 && BN == 64 && kBPer == 4, "kTA layout");
+            int kb0, kb1;
+            k_range(blockIdx.x, kb0, kb1);
+            const int r = q * 32 + lane;
+            const uint32_t aoff = (uint32_t)r * 128u, af = (uint32_t)r & 7u;
+            const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+            for (int j = 0; kb0 + j < kb1; ++j) {
+                const int sp = j % SP, s8 = j % S8;
+                ptx::mbar_wait(&fullP[sp], (uint32_t)(j / SP) & 1u);
+                ptx::mbar_wait(&empty8[s8], ((uint32_t)(j / S8) & 1u) ^ 1u);
+                const uint32_t src = ptx::smem_u32(ringP + sp * Cfg::kStageP);
+                uint4 pa[4], pb[2];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) pa[c] = ptx::lds128(src + aoff + (((uint32_t)(4 * h + c) ^ af) << 4));
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {   // packed W arrives 128-byte swizzled as well
+                    const int id = lane + 32 * (2 * h + i);
+                    const uint32_t rb = (uint32_t)(16 * q + id / kAC), cb = (uint32_t)(id % kAC);
+                    pb[i] = ptx::lds128(src + Cfg::kAP + rb * 128u + ((cb ^ (rb & 7u)) << 4));
+                }
+                uint32_t w[32];
+#pragma unroll
+                for (int cc = 0; cc < 4; ++cc) {
+                    ptx::unpack_i4x8(pa[cc].x, w[8 * cc + 0], w[8 * cc + 4]);
+                    ptx::unpack_i4x8(pa[cc].y, w[8 * cc + 1], w[8 * cc + 5]);
+                    ptx::unpack_i4x8(pa[cc].z, w[8 * cc + 2], w[8 * cc + 6]);
+                    ptx::unpack_i4x8(pa[cc].w, w[8 * cc + 3], w[8 * cc + 7]);
+                }
+                ptx::tmem_st_32x32b_x32(tmem_base + lane_off + Cfg::kTaCol + Cfg::kTaStageCols * (uint32_t)s8 + 32u * (uint32_t)h, w);
+                const uint32_t dst = ptx::smem_u32(ring8 + s8 * Cfg::kStage8 + Cfg::kA8);
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const int id = lane + 32 * (2 * h + i);
+                    const uint32_t rb = (uint32_t)(16 * q + id / kAC), cb = (uint32_t)(id % kAC);
+                    const uint32_t sub = dst + (cb >> 2) * (uint32_t)(BN * 128) + rb * 128u, cl = cb & 3u;
+                    uint4 lo, hi;
+                    ptx::unpack_i4x8(pb[i].x, lo.x, hi.x);
+                    ptx::unpack_i4x8(pb[i].y, lo.y, hi.y);
+                    ptx::unpack_i4x8(pb[i].z, lo.z, hi.z);
+                    ptx::unpack_i4x8(pb[i].w, lo.w, hi.w);
+                    ptx::sts128(sub + (((2u * cl) ^ (rb & 7u)) << 4), lo);
+                    ptx::sts128(sub + (((2u * cl + 1u) ^ (rb & 7u)) << 4), hi);
+                }
+                ptx::tmem_st_wait();             // this thread's A columns are written
+                ptx::fence_proxy_async_smem();   // and its W bytes visible to the tensor core
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    ptx::mbar_arrive(&full8[s8]);
+                    ptx::mbar_arrive(&emptyP[sp]);
+                }
+            }
+        }
+    };
 
     if (warp == 0) {
         // ---------------------------------------------------- TMA producer
@@ -462,6 +532,7 @@ __device__ __forceinline__ void gemm_i8tc_body(const CUtensorMap& tmA, const CUt
     } else if (warp >= 4 && warp < 8) {
         // ---------------------------------------------------- epilogue
         const int q = warp & 3;   // TMEM lane quadrant owned by this warp
+        if constexpr (Cfg::kTA) ta_unpack(q, 1);   // the mainloop's second unpack half first
         int it = 0;
         for (int unit = blockIdx.x; unit < num_tiles; unit += gridDim.x, ++it) {
             const int tile = unit / splits;
@@ -602,75 +673,11 @@ __device__ __forceinline__ void gemm_i8tc_body(const CUtensorMap& tmA, const CUt
         constexpr int kChunks = (BM + BN) * (Cfg::BK / 32);   // 16-byte packed chunks / stage
         static_assert(kChunks % 128 == 0, "chunk split");
         if constexpr (Cfg::kTA) {
-            // Small-M plan, A in TMEM: unpack warp q = warp % 4 owns TMEM lane
-            // quadrant q, i.e. A rows 32q..32q+31 of every stage (lane = row;
-            // packed A arrives with the TMA 128-byte swizzle, so the lanes' row
-            // reads are conflict-free), expands its row's 128 packed bytes in
-            // registers and stores the 256 int8 K bytes with two tcgen05.st
-            // (columns 8c..8c+3 = even codes of packed chunk c, 8c+4..8c+7 = odd
-            // codes: the permutation W gets in shared memory); and it unpacks
-            // W rows 16q..16q+15 into the SW128 sub-tiles (K bytes [128 t,
-            // 128 t + 128) in sub-tile t).
-            constexpr int kAC = Cfg::BK / 32;              // packed 16-byte chunks per row (8)
-            constexpr int kBPer = (BN / 4) * kAC / 32;     // W chunks per lane (4)
-            static_assert(Cfg::BK == 256 && BN == 64, "kTA layout");
+            ta_unpack(warp - 8, 0);
+            // tail: the last MMA commit on slot q has landed
             const int q = warp - 8;
             int kb0, kb1;
             k_range(blockIdx.x, kb0, kb1);
-            const int r = q * 32 + lane;
-            const uint32_t aoff = (uint32_t)r * 128u, af = (uint32_t)r & 7u;
-            const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-            for (int j = 0; kb0 + j < kb1; ++j) {
-                const int sp = j % SP, s8 = j % S8;
-                ptx::mbar_wait(&fullP[sp], (uint32_t)(j / SP) & 1u);
-                ptx::mbar_wait(&empty8[s8], ((uint32_t)(j / S8) & 1u) ^ 1u);
-                const uint32_t src = ptx::smem_u32(ringP + sp * Cfg::kStageP);
-                uint4 pa[kAC], pb[kBPer];
-#pragma unroll
-                for (int c = 0; c < kAC; ++c) pa[c] = ptx::lds128(src + aoff + (((uint32_t)c ^ af) << 4));
-#pragma unroll
-                for (int i = 0; i < kBPer; ++i) {
-                    const int id = lane + 32 * i;
-                    pb[i] = ptx::lds128(src + Cfg::kAP + (uint32_t)(16 * q + id / kAC) * 128u + (uint32_t)(id % kAC) * 16u);
-                }
-                const uint32_t tcol = tmem_base + lane_off + Cfg::kTaCol + Cfg::kTaStageCols * (uint32_t)s8;
-#pragma unroll
-                for (int hlf = 0; hlf < 2; ++hlf) {   // packed chunks 4 hlf .. 4 hlf + 3 -> 32 columns
-                    uint32_t w[32];
-#pragma unroll
-                    for (int cc = 0; cc < 4; ++cc) {
-                        const uint4 p = pa[4 * hlf + cc];
-                        ptx::unpack_i4x8(p.x, w[8 * cc + 0], w[8 * cc + 4]);
-                        ptx::unpack_i4x8(p.y, w[8 * cc + 1], w[8 * cc + 5]);
-                        ptx::unpack_i4x8(p.z, w[8 * cc + 2], w[8 * cc + 6]);
-                        ptx::unpack_i4x8(p.w, w[8 * cc + 3], w[8 * cc + 7]);
-                    }
-                    ptx::tmem_st_32x32b_x32(tcol + 32u * (uint32_t)hlf, w);
-                }
-                const uint32_t dst = ptx::smem_u32(ring8 + s8 * Cfg::kStage8 + Cfg::kA8);
-#pragma unroll
-                for (int i = 0; i < kBPer; ++i) {
-                    const int id = lane + 32 * i;
-                    const uint32_t rb = (uint32_t)(16 * q + id / kAC), cb = (uint32_t)(id % kAC);
-                    const uint32_t sub = dst + (cb >> 2) * (uint32_t)(BN * 128) + rb * 128u, cl = cb & 3u;
-                    uint4 lo, hi;
-                    ptx::unpack_i4x8(pb[i].x, lo.x, hi.x);
-                    ptx::unpack_i4x8(pb[i].y, lo.y, hi.y);
-                    ptx::unpack_i4x8(pb[i].z, lo.z, hi.z);
-                    ptx::unpack_i4x8(pb[i].w, lo.w, hi.w);
-                    ptx::sts128(sub + (((2u * cl) ^ (rb & 7u)) << 4), lo);
-                    ptx::sts128(sub + (((2u * cl + 1u) ^ (rb & 7u)) << 4), hi);
-                }
-                ptx::tmem_st_wait();             // this thread's A columns are written
-                ptx::fence_proxy_async_smem();   // and its W bytes visible to the tensor core
-                ptx::tc_fence_before();
-                __syncwarp();
-                if (lane == 0) {
-                    ptx::mbar_arrive(&full8[s8]);
-                    ptx::mbar_arrive(&emptyP[sp]);
-                }
-            }
-            // tail: the last MMA commit on slot q has landed
             const int n = kb1 - kb0;
             if (q < n) {
                 const int jl = ((n - 1 - q) / S8) * S8 + q;

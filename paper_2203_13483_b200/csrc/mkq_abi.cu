@@ -231,7 +231,7 @@ mkq_status launch_gemm(const void* a, int64_t lda, const void* w, int64_t ldw, i
     // kTA (small-M int4): packed 128-byte A rows with the 128-byte swizzle (conflict-free row reads by lane)
     mkq_status s = make_map(&ma, a, kbytes, (uint64_t)M, (uint64_t)lda, box_in, Cfg::BM, !Cfg::kInt4 || Cfg::kTA);
     if (s != MKQ_OK) return s;
-    s = make_map(&mb, w, kbytes, (uint64_t)N, (uint64_t)ldw, box_in, Cfg::BN, !Cfg::kInt4);
+    s = make_map(&mb, w, kbytes, (uint64_t)N, (uint64_t)ldw, box_in, Cfg::BN, !Cfg::kInt4 || Cfg::kTA);
     if (s != MKQ_OK) return s;
     const int tiles = ((M + Cfg::BM - 1) / Cfg::BM) * ((N + Cfg::BN - 1) / Cfg::BN);
     // output map: TMA stores of the small-M plan's epilogues (unused otherwise)
@@ -421,7 +421,7 @@ mkq_status launch_lnc(const void* a, int64_t lda, const void* w, int64_t ldw, in
     CUtensorMap ma, mb;
     mkq_status s = make_map(&ma, a, (uint64_t)K / 2, (uint64_t)M, (uint64_t)lda, LnCCfg::BK / 2, LnCCfg::BM, true);
     if (s != MKQ_OK) return s;
-    s = make_map(&mb, w, (uint64_t)K / 2, (uint64_t)N, (uint64_t)ldw, LnCCfg::BK / 2, LnCCfg::BN, false);
+    s = make_map(&mb, w, (uint64_t)K / 2, (uint64_t)N, (uint64_t)ldw, LnCCfg::BK / 2, LnCCfg::BN, true);
     if (s != MKQ_OK) return s;
     mkq::LnCParams lp;
     s = make_map_t(&lp.r, ln.res, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (uint64_t)N, (uint64_t)M, (uint64_t)ln.ldr * 4, 32,
