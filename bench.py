@@ -692,8 +692,8 @@ def small_configs(torch, dev, pk, regime):
     tl = graph_time(torch, g, dev, reps=100, inner=20)
     out["c2_bert_base_layer_b1_s128"] = {
         "us_per_layer_single_graph_replay": round(tl1 * 1e3, 2), "us_per_layer_back_to_back": round(tl * 1e3, 2),
-        "effective_tops": round(linear_ops(S, h, Fh) / (tl * 1e-3) / 1e12, 2), "kernels_per_layer": 8,
-        "bound": "latency: 8 dependent kernels at M = 128 (PDL overlaps prologues)"}
+        "effective_tops": round(linear_ops(S, h, Fh) / (tl * 1e-3) / 1e12, 2), "kernels_per_layer": 6 if L.fused_ln(S) else 8,
+        "bound": f"latency: {6 if L.fused_ln(S) else 8} dependent kernels at M = 128 (PDL overlaps prologues)"}
     return out
 
 
