@@ -53,7 +53,7 @@ struct EpiParams {
     int64_t ldo_bytes;
 };
 
-template <int BN_, bool kInt4_>
+template <int BN_, bool kInt4_, bool kSmall_ = false>
 struct GemmCfg {
     static constexpr int BM = 128;
     static constexpr int BN = BN_;
@@ -65,7 +65,7 @@ struct GemmCfg {
     // number of TMA rows in flight, not by bytes (int4 and int8 stages of 128 K
     // both took ~0.35 us with 4 stages in flight, tools/trace_small.py), so
     // 256-K int4 stages halve the time per K
-    static constexpr bool kTA = kInt4 && BN == 64;
+    static constexpr bool kTA = kInt4 && kSmall_;   // (BN 64, or 128 for wider small-M tiles)
     static constexpr int BK = kTA ? 256 : 128;      // K elements per block (=128 int8 bytes/row otherwise)
     static constexpr int kA8 = kTA ? 0 : BM * BK;   // int8 bytes of A per stage (kTA: A lives in TMEM)
     static constexpr int kB8 = BN * BK;             // (kTA: BK/128 SW128 sub-tiles of BN x 128 B)
@@ -73,8 +73,8 @@ struct GemmCfg {
     static constexpr int kAP = BM * BK / 2;         // packed bytes of A per stage
     static constexpr int kBP = BN * BK / 2;
     static constexpr int kStageP = kAP + kBP;
-    static constexpr int S8 = kInt4 ? (BN == 256 ? 3 : 4) : 4;
-    static constexpr int SP = kInt4 ? (BN == 256 ? 3 : 4) : 0;
+    static constexpr int S8 = kInt4 ? ((BN == 256 || (kTA && BN == 128)) ? 3 : 4) : 4;
+    static constexpr int SP = kInt4 ? ((BN == 256 || (kTA && BN == 128)) ? 3 : 4) : 0;
     static_assert(BN == 64 || BN == 128 || BN == 256, "BN");
     static constexpr int kThreads = kInt4 ? 384 : 256;
     static constexpr uint32_t kTaCol = 128;         // first A column (kTA): accumulator in [0, 64)
@@ -385,8 +385,9 @@ __device__ __forceinline__ void gemm_i8tc_body(const CUtensorMap& tmA, const CUt
     auto ta_unpack = [&](int q, int h) {
         if constexpr (Cfg::kTA) {
             constexpr int kAC = Cfg::BK / 32;              // packed 16-byte chunks per row (8)
-            constexpr int kBPer = (BN / 4) * kAC / 32;     // W chunks per lane (4)
-            static_assert(Cfg::BK == 256 && BN == 64 && kBPer == 4, "kTA layout");
+            constexpr int kBPer = (BN / 4) * kAC / 32;     // W chunks per lane (4 for BN 64, 8 for 128)
+            constexpr int kBH = kBPer / 2;                 // per half
+            static_assert(Cfg::BK == 256 && (BN == 64 || BN == 128), "kTA layout");
             int kb0, kb1;
             k_range(blockIdx.x, kb0, kb1);
             const int r = q * 32 + lane;
@@ -397,13 +398,13 @@ __device__ __forceinline__ void gemm_i8tc_body(const CUtensorMap& tmA, const CUt
                 ptx::mbar_wait(&fullP[sp], (uint32_t)(j / SP) & 1u);
                 ptx::mbar_wait(&empty8[s8], ((uint32_t)(j / S8) & 1u) ^ 1u);
                 const uint32_t src = ptx::smem_u32(ringP + sp * Cfg::kStageP);
-                uint4 pa[4], pb[2];
+                uint4 pa[4], pb[kBH];
 #pragma unroll
                 for (int c = 0; c < 4; ++c) pa[c] = ptx::lds128(src + aoff + (((uint32_t)(4 * h + c) ^ af) << 4));
 #pragma unroll
-                for (int i = 0; i < 2; ++i) {   // packed W arrives 128-byte swizzled as well
-                    const int id = lane + 32 * (2 * h + i);
-                    const uint32_t rb = (uint32_t)(16 * q + id / kAC), cb = (uint32_t)(id % kAC);
+                for (int i = 0; i < kBH; ++i) {   // packed W arrives 128-byte swizzled as well
+                    const int id = lane + 32 * (kBH * h + i);
+                    const uint32_t rb = (uint32_t)((BN / 4) * q + id / kAC), cb = (uint32_t)(id % kAC);
                     pb[i] = ptx::lds128(src + Cfg::kAP + rb * 128u + ((cb ^ (rb & 7u)) << 4));
                 }
                 uint32_t w[32];
@@ -417,9 +418,9 @@ __device__ __forceinline__ void gemm_i8tc_body(const CUtensorMap& tmA, const CUt
                 ptx::tmem_st_32x32b_x32(tmem_base + lane_off + Cfg::kTaCol + Cfg::kTaStageCols * (uint32_t)s8 + 32u * (uint32_t)h, w);
                 const uint32_t dst = ptx::smem_u32(ring8 + s8 * Cfg::kStage8 + Cfg::kA8);
 #pragma unroll
-                for (int i = 0; i < 2; ++i) {
-                    const int id = lane + 32 * (2 * h + i);
-                    const uint32_t rb = (uint32_t)(16 * q + id / kAC), cb = (uint32_t)(id % kAC);
+                for (int i = 0; i < kBH; ++i) {
+                    const int id = lane + 32 * (kBH * h + i);
+                    const uint32_t rb = (uint32_t)((BN / 4) * q + id / kAC), cb = (uint32_t)(id % kAC);
                     const uint32_t sub = dst + (cb >> 2) * (uint32_t)(BN * 128) + rb * 128u, cl = cb & 3u;
                     uint4 lo, hi;
                     ptx::unpack_i4x8(pb[i].x, lo.x, hi.x);
@@ -679,7 +680,7 @@ __device__ __forceinline__ void gemm_i8tc_body(const CUtensorMap& tmA, const CUt
             int kb0, kb1;
             k_range(blockIdx.x, kb0, kb1);
             const int n = kb1 - kb0;
-            if (q < n) {
+            if (q < n && q < S8) {
                 const int jl = ((n - 1 - q) / S8) * S8 + q;
                 ptx::mbar_wait(&empty8[q], (uint32_t)(jl / S8) & 1u);
             }
@@ -822,7 +823,7 @@ __device__ __forceinline__ void gemm_i8tc_body(const CUtensorMap& tmA, const CUt
         }
         asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");   // peers have read this CTA's lstat
     }
-    if constexpr (kCl) if (splits > 1) {
+    if constexpr (kCl && Cfg::BN == 64) if (splits > 1) {   // (wider small-M tiles run unsplit)
         // DSMEM reduce-scatter of the staged partials + epilogue (all warps)
         ptx::cluster_sync();   // release/acquire: every peer's staged rows are visible
         const int tile = blockIdx.x / splits;

@@ -353,7 +353,7 @@ mkq_status launch_gemm2_ln_cfg(const void* a, int64_t lda, const void* w, int64_
 int small_m_mode();   // the GEMM plan mode (below)
 
 // ---- small-M fused GEMM + residual + LayerNorm through an N-cluster (kLnC)
-using LnCCfg = mkq::GemmCfg<64, true>;
+using LnCCfg = mkq::GemmCfg<64, true, true>;
 constexpr size_t kLnCSmem = LnCCfg::kSmem + mkq::kLnCExtra;
 
 bool lnc_attrs() {
@@ -485,7 +485,7 @@ int max_clusters(int csize) {
     if (dev < 0 || dev >= 64 || csize < 1 || csize > 8) return 0;
     int& c = cache[dev][csize];
     if (c == 0) {
-        using Cfg = mkq::GemmCfg<64, true>;
+        using Cfg = mkq::GemmCfg<64, true, true>;
         cudaFuncSetAttribute(mkq::gemm_i8tc_kernel<Cfg, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)(csize * 64));
@@ -626,9 +626,15 @@ mkq_status gemm_common(bool int4, const void* a, int64_t lda, const void* w, int
     }
     const SmallPlan sp = plan_small(M, N, K, sms, int4);
     if (sp.use) {
-        if (int4) return launch_gemm<mkq::GemmCfg<64, true>, true>(a, lda, w, ldw, (int)M, (int)N, (int)K, ep, sms, st, sp.splits);
+        if (int4) return launch_gemm<mkq::GemmCfg<64, true, true>, true>(a, lda, w, ldw, (int)M, (int)N, (int)K, ep, sms, st, sp.splits);
         return launch_gemm<mkq::GemmCfg<64, false>, true>(a, lda, w, ldw, (int)M, (int)N, (int)K, ep, sms, st, sp.splits);
     }
+    // int4 small M with more 128 x 64 tiles than SMs (Table-2 QKV at 537-681 tokens):
+    // 128 x 128 tiles of the same A-in-TMEM plan, unsplit, when they fit one wave
+    // (plain outputs; the FFN1 requant keeps the compact-table CTA-pair path)
+    if (int4 && small_m_mode() != 0 && N % 128 == 0 && e.out != MKQ_OUT_I4 && e.out != MKQ_OUT_I8 &&
+        ((M + 127) / 128) * (N / 128) <= sms && ((M + 127) / 128) * ((N + 63) / 64) > sms)
+        return launch_gemm<mkq::GemmCfg<128, true, true>, true>(a, lda, w, ldw, (int)M, (int)N, (int)K, ep, sms, st, 1);
     const bool wide = (N % 256 == 0) && (M > 128 * sms / 2 || (M / 128 + 1) * (N / 256) >= sms);
     static const int path_override = [] {   // MKQ_GEMM_PATH=1cta|2cta (diagnostics)
         const char* v = getenv("MKQ_GEMM_PATH");

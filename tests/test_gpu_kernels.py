@@ -155,6 +155,30 @@ def test_gemm_float_epilogues_bitexact(bits, mode, gelu, small_mode):
         assert np.array_equal(out.view(np.uint16), ref.view(np.uint16))
 
 
+# int4 small M with more 128 x 64 tiles than SMs but 128 x 128 tiles in one
+# wave (Table-2 QKV at 537-681 tokens): the 128 x 128 A-in-TMEM plan, every
+# plain output mode (GELU included) and the raw accumulators
+@pytest.mark.parametrize("Mm,N,K", [(681, 2304, 768), (900, 1280, 1024), (537, 2304, 96)])
+@pytest.mark.parametrize("mode", [M.OUT_F32, M.OUT_F16, M.OUT_BF16, M.OUT_I32])
+def test_gemm_small_m_wide_tiles(Mm, N, K, mode):
+    rng = np.random.default_rng(Mm + N + K + mode)
+    A, W = _codes(rng, Mm, N, K, 4)
+    s_a = np.float32(0.5558)
+    s_w = rng.uniform(1e-3, 1e-2, N).astype(np.float32)
+    b = rng.uniform(-0.1, 0.1, N).astype(np.float32)
+    gelu = mode == M.OUT_F32
+    out = host(_run(4, A, W, s_a, s_w, b, mode=mode, gelu=gelu))
+    if mode == M.OUT_I32:
+        assert np.array_equal(out, oracle.gemm_i32(A, W))
+        return
+    omode = {M.OUT_F32: oracle.OUT_F32, M.OUT_F16: oracle.OUT_F16, M.OUT_BF16: oracle.OUT_BF16}[mode]
+    ref = oracle.linear(A, W, s_a, s_w, b, mode=omode, gelu=gelu)
+    if mode == M.OUT_F32:
+        assert np.array_equal(out.view(np.uint32), ref.view(np.uint32))
+    else:
+        assert np.array_equal(out.view(np.uint16), ref.view(np.uint16))
+
+
 @pytest.mark.parametrize("bits", [4, 8])
 @pytest.mark.parametrize("Mm,N,K", [(1, 32, 64), (128, 3072, 768), (257, 4096, 1024)])
 def test_gemm_requant_gelu_bitexact(bits, Mm, N, K, small_mode):
