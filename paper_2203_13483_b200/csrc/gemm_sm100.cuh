@@ -759,10 +759,12 @@ __device__ __forceinline__ void gemm_i8tc_body(const CUtensorMap& tmA, const CUt
                     mean = o.x;
                     M2 = o.y;
                 } else {   // equal counts 64: Chan et al.'s pairwise update
+                    // (pc is a compile-time constant in the unrolled loop: both IEEE
+                    // quotients fold to constants instead of a dependent division chain)
                     const float d = __fsub_rn(o.x, mean);
                     const float nt = (float)(64 * (pc + 1)), nw = (float)(64 * pc);
-                    mean = __fadd_rn(mean, __fmul_rn(d, __fdiv_rn(64.0f, nt)));
-                    M2 = __fadd_rn(__fadd_rn(M2, o.y), __fmul_rn(__fmul_rn(d, d), __fdiv_rn(nw * 64.0f, nt)));
+                    mean = __fadd_rn(mean, __fmul_rn(d, 64.0f / nt));
+                    M2 = __fadd_rn(__fadd_rn(M2, o.y), __fmul_rn(__fmul_rn(d, d), (nw * 64.0f) / nt));
                 }
             }
             const float rstd = rsqrtf(__fadd_rn(__fdiv_rn(M2, (float)N), lp->eps));
