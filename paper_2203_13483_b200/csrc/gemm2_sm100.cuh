@@ -582,7 +582,7 @@ __device__ __forceinline__ void ln_epilogue(const Epi2Params& p, const LnMaps& l
 #pragma unroll
         for (int i = 0; i < kCW; i += 2) sp[(i >> 1) & 3] = add2(sp[(i >> 1) & 3], make_float2(r[i], r[i + 1]));
         const float2 s2 = add2(add2(sp[0], sp[1]), add2(sp[2], sp[3]));
-        const float mw = __fdiv_rn(__fadd_rn(s2.x, s2.y), (float)kCW);
+        const float mw = __fdiv_rn(__fadd_rn(s2.x, s2.y), (float)kCW);   // kCW constant: folds to a multiply
 #pragma unroll
         for (int k = 0; k < 4; ++k) sp[k] = make_float2(0.f, 0.f);
 #pragma unroll
@@ -610,9 +610,11 @@ __device__ __forceinline__ void ln_epilogue(const Epi2Params& p, const LnMaps& l
             for (int w = 1; w < kQW; ++w) {   // equal counts kCW: pairwise update
                 const float2 o = qpart[w * BM + row_l];
                 const float d = __fsub_rn(o.x, c.x);
+                // (w is a compile-time constant in the unrolled loop: the IEEE
+                // quotients fold to constants, no dependent division chain)
                 const float nw = (float)(w * kCW), nt = (float)((w + 1) * kCW);
-                c.x = __fadd_rn(c.x, __fmul_rn(d, __fdiv_rn((float)kCW, nt)));
-                c.y = __fadd_rn(__fadd_rn(c.y, o.y), __fmul_rn(__fmul_rn(d, d), __fdiv_rn(nw * (float)kCW, nt)));
+                c.x = __fadd_rn(c.x, __fmul_rn(d, (float)kCW / nt));
+                c.y = __fadd_rn(__fadd_rn(c.y, o.y), __fmul_rn(__fmul_rn(d, d), (nw * (float)kCW) / nt));
             }
             const uint64_t word = (uint64_t)__float_as_uint(c.x) | ((uint64_t)(__float_as_uint(c.y) | (tag << 31)) << 32);
             st_relaxed_gpu_u64(slot + (size_t)j * (2 * BM) + rank * BM + row_l, word);
@@ -644,9 +646,9 @@ __device__ __forceinline__ void ln_epilogue(const Epi2Params& p, const LnMaps& l
         for (int jj = 1; jj < 4; ++jj) {   // column tiles in order: pairwise update, counts BN
             if (jj < np) {
                 const float d = __fsub_rn(part[jj].x, mean);
-                const float nw = (float)(jj * BN), nt = (float)((jj + 1) * BN);
-                mean = __fadd_rn(mean, __fmul_rn(d, __fdiv_rn((float)BN, nt)));
-                M2 = __fadd_rn(__fadd_rn(M2, part[jj].y), __fmul_rn(__fmul_rn(d, d), __fdiv_rn(nw * (float)BN, nt)));
+                const float nw = (float)(jj * BN), nt = (float)((jj + 1) * BN);   // constants (unrolled)
+                mean = __fadd_rn(mean, __fmul_rn(d, (float)BN / nt));
+                M2 = __fadd_rn(__fadd_rn(M2, part[jj].y), __fmul_rn(__fmul_rn(d, d), (nw * (float)BN) / nt));
             }
         }
         const float rstd = rsqrtf(__fadd_rn(__fdiv_rn(M2, (float)N), L.eps));
