@@ -28,9 +28,21 @@
 //   warp 2      TMEM allocator
 //   warps 4-7   epilogue: tcgen05.ld 32x32b -> dequant/GELU/requant -> global
 //   warps 8-11  int4 -> int8 unpack (W4A4 only)
+//   warp 3      (small-M plans) column scales / bias (/ LN gamma, beta) -> smem
 // Pipelines: packed ring (TMA -> unpack), int8 ring (unpack|TMA -> MMA),
 // double-buffered TMEM accumulators (MMA -> epilogue), so the epilogue of
 // tile i overlaps the mainloop of tile i+1.
+//
+// Small-M plans (kCl: one tile per CTA, the paper's Table-2 regime):
+//   * int4 (GemmCfg<BN, true, true>, kTA): 256-K stages; A is unpacked into
+//     tensor memory (lane = row, tcgen05.st) by warps 8-11 and 4-7 (one half
+//     of each stage each) and read by the MMA from there; W unpacks to the
+//     SW128 ring.  BN 64 (K split over a cluster for long K) or 128.
+//   * the unsplit epilogue stages 32-row blocks and TMA-stores them; the K
+//     split reduces exact int32 partials over DSMEM first.
+//   * kLnC (gemm_lnc_kernel): an N-cluster of N/64 CTAs per 128-row block adds
+//     the residual and applies LayerNorm (+ Eq.1 codes) with row statistics
+//     exchanged over DSMEM.
 #pragma once
 #include <cstdint>
 #include <cuda.h>
