@@ -225,20 +225,32 @@ __global__ void __launch_bounds__(kThreads) flash_attn_kernel(const Params p) {
         l_r[h] += __shfl_xor_sync(0xffffffffu, l_r[h], 2);
     }
     const float inv[2] = {1.0f / l_r[0], 1.0f / l_r[1]};
+    const QuantRcp Qo = quant_rcp(p.out_mode ? p.s_out : 1.0f, p.qmin, p.qmax);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
         const int r = q0 + warp * 16 + (lane >> 2) + 8 * h;
         if (r >= len) continue;
         uint8_t* orow = reinterpret_cast<uint8_t*>(p.out) + (int64_t)(start + r) * p.ldo;
+        float v[16];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-            const int col = head * kD + i * 8 + 2 * (lane & 3);
-            const float v0 = o[i][2 * h] * inv[h], v1 = o[i][2 * h + 1] * inv[h];
-            if (p.out_mode == 0) {
-                *reinterpret_cast<float2*>(orow + (int64_t)col * 4) = make_float2(v0, v1);
-            } else {
-                const int c0 = quant_code(v0, p.s_out, p.qmin, p.qmax);
-                const int c1 = quant_code(v1, p.s_out, p.qmin, p.qmax);
+            v[2 * i] = o[i][2 * h] * inv[h];
+            v[2 * i + 1] = o[i][2 * h + 1] * inv[h];
+        }
+        if (p.out_mode == 0) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                *reinterpret_cast<float2*>(orow + (int64_t)(head * kD + i * 8 + 2 * (lane & 3)) * 4) =
+                    make_float2(v[2 * i], v[2 * i + 1]);
+        } else {
+            // Eq.1 via the reciprocal, the exact division only for a group with a
+            // value near a rounding boundary (epilogue.cuh; was 16 IEEE divisions)
+            int cq[16];
+            quant_group_rcp(v, Qo, cq);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int col = head * kD + i * 8 + 2 * (lane & 3);
+                const int c0 = cq[2 * i], c1 = cq[2 * i + 1];
                 if (p.out_mode == 3) {
                     orow[col >> 1] = (uint8_t)((c0 & 0xF) | ((c1 & 0xF) << 4));
                 } else {
