@@ -124,25 +124,27 @@ __device__ __forceinline__ void epilogue_emit(const EpiParams& ep, float (&y)[32
         break;
     }
     case OUT_I4: {
+        // Eq.1 via the reciprocal; a group with a value near a rounding
+        // boundary takes the exact division (quant_group_rcp, bit-identical)
+        int q[32];
+        quant_group_rcp(y, quant_rcp(ep.s_out, ep.qmin, ep.qmax), q);
         uint32_t w[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            int q[8];
+            int q8[8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) q[j] = quant_code(y[8 * i + j], ep.s_out, ep.qmin, ep.qmax);
-            w[i] = pack_nib8(q);
+            for (int j = 0; j < 8; ++j) q8[j] = q[8 * i + j];
+            w[i] = pack_nib8(q8);
         }
         *reinterpret_cast<uint4*>(orow + n / 2) = make_uint4(w[0], w[1], w[2], w[3]);
         break;
     }
     case OUT_I8: {
+        int q[32];
+        quant_group_rcp(y, quant_rcp(ep.s_out, ep.qmin, ep.qmax), q);   // (as OUT_I4)
         uint32_t w[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
-            w[i] = pack_byte4(quant_code(y[4 * i], ep.s_out, ep.qmin, ep.qmax),
-                              quant_code(y[4 * i + 1], ep.s_out, ep.qmin, ep.qmax),
-                              quant_code(y[4 * i + 2], ep.s_out, ep.qmin, ep.qmax),
-                              quant_code(y[4 * i + 3], ep.s_out, ep.qmin, ep.qmax));
+        for (int i = 0; i < 8; ++i) w[i] = pack_byte4(q[4 * i], q[4 * i + 1], q[4 * i + 2], q[4 * i + 3]);
         uint4* o = reinterpret_cast<uint4*>(orow + n);
         o[0] = make_uint4(w[0], w[1], w[2], w[3]);
         o[1] = make_uint4(w[4], w[5], w[6], w[7]);
@@ -235,25 +237,27 @@ __device__ __forceinline__ void epilogue_acc_stage(const EpiParams& ep, const in
         break;
     }
     case OUT_I4: {
+        // Eq.1 via the reciprocal; a group with a value near a rounding
+        // boundary takes the exact division (quant_group_rcp, bit-identical)
+        int q[32];
+        quant_group_rcp(y, quant_rcp(ep.s_out, ep.qmin, ep.qmax), q);
         uint32_t w[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            int q[8];
+            int q8[8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) q[j] = quant_code(y[8 * i + j], ep.s_out, ep.qmin, ep.qmax);
-            w[i] = pack_nib8(q);
+            for (int j = 0; j < 8; ++j) q8[j] = q[8 * i + j];
+            w[i] = pack_nib8(q8);
         }
         *reinterpret_cast<uint4*>(stage + stage_off(r, 0, 16)) = make_uint4(w[0], w[1], w[2], w[3]);
         break;
     }
     case OUT_I8: {
+        int q[32];
+        quant_group_rcp(y, quant_rcp(ep.s_out, ep.qmin, ep.qmax), q);   // (as OUT_I4)
         uint32_t w[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
-            w[i] = pack_byte4(quant_code(y[4 * i], ep.s_out, ep.qmin, ep.qmax),
-                              quant_code(y[4 * i + 1], ep.s_out, ep.qmin, ep.qmax),
-                              quant_code(y[4 * i + 2], ep.s_out, ep.qmin, ep.qmax),
-                              quant_code(y[4 * i + 3], ep.s_out, ep.qmin, ep.qmax));
+        for (int i = 0; i < 8; ++i) w[i] = pack_byte4(q[4 * i], q[4 * i + 1], q[4 * i + 2], q[4 * i + 3]);
         *reinterpret_cast<uint4*>(stage + stage_off(r, 0, 32)) = make_uint4(w[0], w[1], w[2], w[3]);
         *reinterpret_cast<uint4*>(stage + stage_off(r, 1, 32)) = make_uint4(w[4], w[5], w[6], w[7]);
         break;
