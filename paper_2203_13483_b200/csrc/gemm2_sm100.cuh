@@ -582,7 +582,7 @@ __device__ __forceinline__ void ln_epilogue(const Epi2Params& p, const LnMaps& l
 #pragma unroll
         for (int i = 0; i < kCW; i += 2) sp[(i >> 1) & 3] = add2(sp[(i >> 1) & 3], make_float2(r[i], r[i + 1]));
         const float2 s2 = add2(add2(sp[0], sp[1]), add2(sp[2], sp[3]));
-        const float mw = __fdiv_rn(__fadd_rn(s2.x, s2.y), (float)kCW);   // kCW constant: folds to a multiply
+        const float mw = __fadd_rn(s2.x, s2.y) / (float)kCW;   // IEEE; kCW a power of two: an exact multiply
 #pragma unroll
         for (int k = 0; k < 4; ++k) sp[k] = make_float2(0.f, 0.f);
 #pragma unroll

@@ -597,7 +597,7 @@ __device__ __forceinline__ void gemm_i8tc_body(const CUtensorMap& tmA, const CUt
                         for (int i = 8; i < 64; ++i) ps[i & 7] = __fadd_rn(ps[i & 7], rr[i]);
                         const float sum = __fadd_rn(__fadd_rn(__fadd_rn(ps[0], ps[1]), __fadd_rn(ps[2], ps[3])),
                                                     __fadd_rn(__fadd_rn(ps[4], ps[5]), __fadd_rn(ps[6], ps[7])));
-                        const float mean = __fdiv_rn(sum, 64.0f);
+                        const float mean = sum / 64.0f;   // IEEE; an exact multiply by 2^-6
 #pragma unroll
                         for (int k = 0; k < 8; ++k) {
                             const float d = __fsub_rn(rr[k], mean);
