@@ -323,6 +323,23 @@ def test_layer_table2_bert_base_varlen(bits):
     _stagewise_sampled(L, _oracle_weights(p, bits, L.scales), h, 16, S, seqlens, cu, list(range(16)))
 
 
+def test_layer_bert_large_small_batch_fused_ln_cluster():
+    """BERT-large width at a small token count (3 sequences of 150 / 97 / 53
+    tokens): W^A + LN1 and W^2 + LN2 run as the small-M N-cluster kernel with
+    16-CTA clusters (hidden 1024), attention through the tcgen05 kernel
+    (max_seq > 128); stage-wise on every row."""
+    hidden, heads, ffn, S = 1024, 16, 4096, 150
+    p = synth.layer_params(hidden, heads, ffn, 0)
+    L = model.build_layer(p, 4, DEV)
+    model.calibrate(L, dev(synth.hidden_states(2, S, hidden, seed=1000000)), 2, S)
+    seqlens = [150, 97, 53]
+    T = sum(seqlens)
+    assert L.fused_ln(T)
+    h = synth.hidden_states(1, T, hidden, seed=3)
+    cu = dev(np.concatenate([[0], np.cumsum(seqlens)]).astype(np.int32))
+    _stagewise_sampled(L, _oracle_weights(p, 4, L.scales), h, 3, S, seqlens, cu, [0, 1, 2])
+
+
 def test_layer_bert_large_full_batch_sampled_sequence():
     """BASELINE configs[3] at full size (BERT-large, batch 256 x seq 512 =
     131072 tokens, bench.py's call): stage-wise on two sampled sequences
